@@ -1,0 +1,477 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 data-parallel hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1, one rank per GPU)
+
+Workload -- BASELINE.json configs[4] ("C5"), the only config quoted at 1 GPU:
+one synthetic data-parallel SGD iteration per step on every GPU:
+  1. DIMD minibatch: 32 records of 224x224x3 uint8 drawn from the GPU-resident
+     shard (160,000 records = 24.08 GB per GPU, the C4 shard size) with the
+     reference's Philox stream (random_batch, dimd.py:213-220) and gathered;
+  2. synthetic gradient producer: the reference benchmark's deterministic
+     per-rank fill (bench.py:188-195) of the 25.6M(+2) float gradient -- a
+     stand-in for the ResNet-50 backward pass, which is outside the hot path;
+  3. ONE fused launch: multicolor allreduce (k colors, reference trees) + SGD
+     momentum 0.9 / weight decay 1e-4 update of the replicated weights.
+``value`` = whole-job samples/s (N x 32 / step time), inputs resident in HBM,
+CUDA events on the rank's stream, max over ranks. ``step_ms`` is the SGD step
+time and ``allreduce.bus_gbps`` the multi-color allreduce bus bandwidth
+(2 P (N-1)/N / t, the reference's formula, src/bench.py:116-119) -- the two
+quantities BASELINE.json's metric names. ``e2e`` repeats the step through the
+public API with the gradient arriving from pinned host memory every step and
+the loss/labels read back. Inputs (W, momentum, gradient: 307 MB per GPU)
+exceed the 126 MB L2, so no flush is needed between steps.
+
+``--impl reference`` times the reference algorithm on the host CPU: the C
+port in oracle/ (the reference itself is Python over an emulated transport
+and cannot run on the GPU box), rank 0 only, all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+P = 25_600_000            # ResNet-50 gradient floats (BASELINE.json)
+REC = 224 * 224 * 3       # 150,528-byte records
+BATCH = 32                # per GPU
+SHARD = int(os.environ.get("MD_BENCH_SHARD", "160000"))
+MOM, WD, BASE_LR = 0.9, 1e-4, 0.1
+SEED = 2017
+METRIC = "multi-color allreduce bus GB/s (25.6M fp32) at 1/2/4/8 B200; SGD step ms"
+NVLINK_PEAK = 770.0       # measured peer copy GB/s/direction (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0
+HBM_FALLBACK = 6650.0
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak() -> tuple[float, str]:
+    f = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(f.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:  # noqa: BLE001
+        return HBM_FALLBACK, "B200_PROFILING.md fallback"
+
+
+def tree_config(n: int):
+    """The reference's default plan (sgd.py:453-467 comm_plan): widest k."""
+    from paper_1711_00705_b200.sgd import comm_plan
+
+    ts, _ = comm_plan(n, "multicolor")
+    return ts
+
+
+# -- clocks ---------------------------------------------------------------------------------------
+
+
+class Clocks:
+    """nvidia-smi sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                if int(r[0]) not in self.gpus:
+                    continue
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -- our implementation ------------------------------------------------------------------------------
+
+
+def run_ours(a) -> None:
+    import torch
+
+    from paper_1711_00705_b200 import _lib, dimd
+    from paper_1711_00705_b200.collectives import GradientBuffer, SgdUpdate, allreduce
+    from paper_1711_00705_b200.dimd import BatchRequest, BatchSlots, random_batch_device
+    from paper_1711_00705_b200.sgd import (
+        SAMPLE_ROLE, DeviceModel, TrainConfig, check_replicas, lr_at, lr_schedule)
+    from paper_1711_00705_b200.transport import init_from_env
+
+    ep = init_from_env()
+    N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
+    if N != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={N}")
+    lib = _lib.load()
+    stream = ep.stream
+    sptr = _lib.stream_ptr(stream)
+    ts = tree_config(N)
+    cfg = TrainConfig(n_nodes=N, workers_per_node=1, per_worker_batch=BATCH, epochs=90,
+                      momentum=MOM, weight_decay=WD, base_lr=BASE_LR, seed=SEED)
+    B = cfg.effective_batch
+    lr = lr_at(lr_schedule(cfg), 10.0)
+
+    with torch.cuda.stream(stream):
+        store = dimd.synth_store(SHARD, REC, rank, N, SEED, 0, N, rank, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(SEED)  # identical replicas on every rank
+        w = torch.randn(P, generator=g, device=dev) * 0.01
+        model = DeviceModel(w, torch.zeros_like(w))
+        grad = GradientBuffer.alloc(P + 2, ep)
+        slots = BatchSlots(BATCH, REC, dev)
+        upd = SgdUpdate(weights=model.weights, c=lr / B, momentum=model.momentum, mu=MOM,
+                        wd_b=WD * B, update_len=P)
+    torch.cuda.synchronize(dev)
+
+    def fill():
+        _lib.check(lib.md_fill_rank_input(grad.data.data_ptr(), P + 2, rank, N, sptr))
+
+    ar_ev = []
+
+    def step(i, timed=False):
+        key = dimd._mix64(SEED, SAMPLE_ROLE, rank, i)
+        random_batch_device(store, BatchRequest(BATCH, key), REC, slots)
+        fill()
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
+        if timed:
+            e1.record(stream)
+            ar_ev.append((e0, e1))
+
+    with torch.cuda.stream(stream):
+        # correctness before timing (reference bench.py:198-212 + 258-268):
+        # closed-form f64 sum of the fill, rel err <= 1e-5
+        step(0)
+        ep.synchronize()
+        slots.check()
+        idx = np.arange(0, P, 7919)
+        got = grad.data[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
+        total = sum((r + 1) * np.pi / N for r in range(N))
+        want = (idx.astype(np.float64) % 997.0 + 1.0) * total
+        rel = float(np.max(np.abs(got - want) / np.abs(want)))
+        if rel > 1e-5:
+            raise SystemExit(f"allreduce result check failed: max rel err {rel:.3g}")
+        for i in range(1, a.warmup + 1):
+            step(i)
+        ep.synchronize()
+
+        ep.barrier()
+        torch.cuda.synchronize(dev)
+        clocks = Clocks(list(range(N))) if rank == 0 else None
+        if clocks:
+            clocks.start()
+        l0 = lib.md_launch_count()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(a.steps):
+            step(a.warmup + 1 + i, timed=True)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        launches = lib.md_launch_count() - l0
+        ep.barrier()
+        clk = clocks.stop() if clocks else None
+        ep.take_error()
+        slots.check()
+        ms = t0.elapsed_time(t1)
+        ar_ms = sum(e0.elapsed_time(e1) for e0, e1 in ar_ev) / len(ar_ev)
+        check_replicas(ep, model.weights, a.steps)
+
+        # -- end to end through the public API, host buffers --------------------------------
+        e2e = None
+        if not a.no_e2e:
+            host = torch.empty(P + 2, dtype=torch.float32).pin_memory()
+            host.copy_(torch.from_numpy(_host_fill(P + 2, rank, N)))
+            out_tail = torch.empty(2, dtype=torch.float32).pin_memory()
+            out_lab = torch.empty(BATCH, dtype=torch.int32).pin_memory()
+
+            def e2e_step(i):
+                grad.data.copy_(host, non_blocking=True)                      # H2D
+                key = dimd._mix64(SEED, SAMPLE_ROLE, rank, i)
+                random_batch_device(store, BatchRequest(BATCH, key), REC, slots)
+                allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
+                out_tail.copy_(grad.data[P:P + 2], non_blocking=True)       # D2H result
+                out_lab.copy_(slots.labels, non_blocking=True)
+                stream.synchronize()                                         # user reads loss
+                return float(out_tail[0])
+
+            for i in range(a.warmup):
+                e2e_step(10_000 + i)
+            ep.barrier()
+            torch.cuda.synchronize(dev)
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for i in range(a.steps):
+                e2e_step(20_000 + i)
+            s1.record(stream)
+            torch.cuda.synchronize(dev)
+            ep.barrier()
+            ep.take_error()
+            e2e_ms = s0.elapsed_time(s1)
+            e2e = (e2e_ms, (P + 2) * 4, 2 * 4 + BATCH * 4)
+
+    rows = ep.all_gather((ms, ar_ms, launches, e2e))
+    if rank != 0:
+        return
+    ms = max(r[0] for r in rows)
+    ar_ms = max(r[1] for r in rows)
+    launches = sum(r[2] for r in rows)
+    step_ms = ms / a.steps
+    value = N * BATCH / (step_ms / 1e3)
+    bus = 2.0 * P * 4 * (N - 1) / N / (ar_ms / 1e3) / 1e9 if N > 1 else None
+    peak_hbm, peak_src = hbm_peak()
+    if N > 1:
+        achieved = bus
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK, "unit": "GB/s",
+                "frac": achieved / NVLINK_PEAK,
+                "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
+                "algorithmic_bytes_per_launch": 2 * P * 4 * (N - 1) / N,
+                "kernel": "md::allreduce_kernel<4> (fused multicolor allreduce + SGD)"}
+    else:
+        # lone rank: the fused kernel is the momentum/wd update: read g, r/w W and v
+        algo_bytes = P * 20
+        achieved = algo_bytes / (ar_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                "frac": achieved / peak_hbm, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": algo_bytes,
+                "kernel": "md::allreduce_kernel<4> (N=1: fused SGD momentum+wd epilogue)"}
+    roof["traffic"] = _ncu_traffic(N)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "samples/s",
+        "n_gpus": N,
+        "steps": a.steps,
+        "warmup": a.warmup,
+        "ms_per_step": step_ms,
+        "step_ms": step_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (device-generated 224x224x3 uint8 records; deterministic fill "
+                "gradient; random-init weights)",
+        "config": {
+            "workload": "C5: DIMD gather 32 rec/GPU + synthetic 25.6M-float gradient + fused "
+                        "multicolor allreduce + SGD(momentum 0.9, wd 1e-4), per step",
+            "global_batch": N * BATCH, "per_gpu_batch": BATCH, "record_bytes": REC,
+            "shard_records_per_gpu": SHARD, "params": P, "algo": "multicolor",
+            "k_colors": ts.k if ts else 1, "arity": ts.arity if ts else None,
+            "parallelism": f"dp{N}",
+            "l2": "inputs larger than L2 (W + momentum + gradient = 307 MB per GPU)",
+        },
+        "allreduce": {"ms": ar_ms, "bus_gbps": bus,
+                      "frac_of_770": (bus / NVLINK_PEAK) if bus else None,
+                      "frac_of_900": (bus / NVLINK_NOMINAL) if bus else None},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if e2e is not None and all(r[3] for r in rows):
+        e2e_ms = max(r[3][0] for r in rows) / a.steps
+        line["e2e"] = {"value": N * BATCH / (e2e_ms / 1e3), "unit": "samples/s",
+                       "ms_per_step": e2e_ms, "h2d_bytes_per_step": e2e[1],
+                       "d2h_bytes_per_step": e2e[2]}
+    if N == 1 and not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_port(N, steps=3)
+    print(json.dumps(line), flush=True)
+
+
+def _host_fill(n: int, rank: int, n_ranks: int) -> np.ndarray:
+    scale = (rank + 1) * np.pi / n_ranks
+    return ((np.arange(n, dtype=np.float64) % 997.0 + 1.0) * scale).astype(np.float32)
+
+
+def _ncu_traffic(n: int):
+    f = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(f.read_text()).get(str(n))
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# -- CPU baseline / reference arm (oracle port) -------------------------------------------------------
+
+
+def cpu_step_port(n_ranks: int, state: dict, step: int, threads: int) -> None:
+    """One C5 step for every rank, on the host, with the oracle's C port."""
+    import ctypes as C
+
+    from oracle import oracle as O
+
+    L = O.lib()
+    for r in range(n_ranks):
+        picks = O.integers_c(O.mix64(SEED, O.SAMP_ROLE, r, step), SHARD, BATCH)
+        src = state["shard"]
+        for j, pk in enumerate(picks):
+            k = int(pk) % state["shard_n"]  # bounded host shard (see sample text)
+            state["batch"][j] = src[k]
+        _par_fill(L, state["grads"][r], r, n_ranks, threads)
+    O.allreduce_threads(state["tables"], state["grads"], weights=state["w"], moms=state["v"],
+                        update_len=P, c=state["c"], mu=MOM, wd_b=state["wd_b"], threads=threads)
+    assert C
+
+
+def _par_fill(L, buf, rank, n_ranks, threads):
+    """mo_fill_rank_input over T ranges (ctypes drops the GIL)."""
+    import ctypes as C
+
+    n = len(buf)
+    per = (n + threads - 1) // threads
+    scale = (rank + 1) * np.pi / n_ranks
+
+    def work(t):
+        lo, hi = t * per, min(n, (t + 1) * per)
+        if lo < hi:
+            idx = np.arange(lo, hi, dtype=np.float64)
+            buf[lo:hi] = ((idx % 997.0 + 1.0) * scale).astype(np.float32)
+
+    ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert C and L
+
+
+def _cpu_state(n_ranks: int):
+    from oracle import oracle as O
+
+    from paper_1711_00705_b200.sgd import TrainConfig, lr_at, lr_schedule
+
+    ts = tree_config(n_ranks)
+    if ts is None:
+        tables = (np.array([-1], np.int32), np.array([0, 0], np.int32), np.zeros(0, np.int32),
+                  np.zeros(1, np.int32))
+    else:
+        tables = O.tables_from_trees(n_ranks, O.trees(n_ranks, ts.k, ts.arity))
+    cfg = TrainConfig(n_nodes=n_ranks, workers_per_node=1, per_worker_batch=BATCH, epochs=90,
+                      momentum=MOM, weight_decay=WD, base_lr=BASE_LR, seed=SEED)
+    B = cfg.effective_batch
+    rng = np.random.default_rng(SEED)
+    shard_n = 512
+    return {
+        "tables": tables,
+        "grads": [np.zeros(P + 2, np.float32) for _ in range(n_ranks)],
+        "w": [(rng.standard_normal(P, dtype=np.float32) * 0.01) for _ in range(1)] * n_ranks,
+        "v": [np.zeros(P, np.float32) for _ in range(n_ranks)],
+        "shard": rng.integers(0, 256, size=(shard_n, REC), dtype=np.uint8),
+        "shard_n": shard_n,
+        "batch": np.empty((BATCH, REC), np.uint8),
+        "c": float(np.float32(lr_at(lr_schedule(cfg), 10.0) / B)),
+        "wd_b": float(np.float32(WD * B)),
+    }
+
+
+def cpu_baseline_port(n_ranks: int, steps: int = 3) -> dict:
+    threads = len(os.sched_getaffinity(0))
+    st = _cpu_state(n_ranks)
+    st["w"] = [w.copy() for w in st["w"]]
+    cpu_step_port(n_ranks, st, 0, threads)  # warm (page faults)
+    t0 = time.perf_counter()
+    for s in range(steps):
+        cpu_step_port(n_ranks, st, 1 + s, threads)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": n_ranks * BATCH / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "ms_per_step": dt * 1e3,
+            "sample": f"{steps} full C5 steps for {n_ranks} rank(s) on the host: 32-record gather "
+                      f"(picks from the reference Philox stream, records from a 512-record host "
+                      f"shard), deterministic gradient fill, tree-order fold + broadcast + fused "
+                      f"SGD(momentum, wd) over 25.6M floats per rank (oracle/mdoracle.c, "
+                      f"{threads} threads)"}
+
+
+def run_reference(a) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    N = a.gpus
+    threads = len(os.sched_getaffinity(0))
+    st = _cpu_state(N)
+    st["w"] = [w.copy() for w in st["w"]]
+    for i in range(a.warmup):
+        cpu_step_port(N, st, i, threads)
+    t0 = time.perf_counter()
+    for i in range(a.steps):
+        cpu_step_port(N, st, a.warmup + i, threads)
+    dt = (time.perf_counter() - t0) / a.steps
+    v = N * BATCH / dt
+    sample = (f"C5 step for all {N} ranks emulated on the host (rank 0 only): picks from the "
+              f"reference Philox stream, 32 x 150528-byte record gather per rank, gradient fill, "
+              f"tree-order multicolor fold + broadcast, fused SGD(momentum, wd) of 25.6M floats "
+              f"per rank; oracle/mdoracle.c C port of the reference algorithm, {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": N,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": "C5 (see bench.py docstring), CPU port",
+                                         "global_batch": N * BATCH, "parallelism": f"dp{N}"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main() -> None:
+    a = args_()
+    a.warmup = max(3, a.warmup)  # timing rule: at least 3 untimed warm-up steps
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,985 @@
+// Multi-color tree allreduce over NVLink/NVSwitch peer memory (sm_100a).
+//
+// Reference semantics (/root/reference/pkg/src/minidist/collectives.py):
+//   * allreduce_multicolor (:225-268): the payload is split into k contiguous
+//     chunks (make_chunk_plan, topology.py:103-120); chunk c is reduced up
+//     color tree c -- every node folds, IN CHILD-LIST ORDER, its own value and
+//     its children's subtree sums (_tree_up_task, :271-286) -- and the root's
+//     result is broadcast back down the same tree (_tree_down_task, :289-296).
+//   * allreduce_ring (:302-359) is the same fold on a chain (each node folds
+//     its successor), reduce_then_broadcast (:365-409) a star whose root folds
+//     every rank in ascending rank order. All three are one kernel here; the
+//     fold tree is data (md_plan_t).
+//
+// B200 design: ONE persistent kernel per call and rank. CTAs pull work items
+// (task, segment) from a per-rank queue ordered (segment, pipeline stage);
+// an UP item loads the children's segments straight out of the peers' HBM
+// over NVLink (16-byte vector loads, all children's loads in flight), folds
+// them in registers in the reference's order with __fadd_rn (no FMA), stores
+// the subtree sum in place, and releases a per-(color, segment) flag in the
+// parent's control block; a DOWN item copies the parent's final segment. The
+// optional prologue folds per-worker gradient buffers (sgd.py:335-353) into
+// the own value on the fly, and the optional epilogue applies the SGD
+// (momentum / weight-decay) update to the replicated weights as soon as a
+// segment's sum is final, so the gradient is never re-read from HBM.
+//
+// Synchronisation (replaces the transport's expose/pull and the length-header
+// barrier of _check_same_length, :157-174): epoch-tagged flags in peer-mapped
+// control blocks, written with st.release.sys after __threadfence_system and
+// polled with ld.acquire.sys; an entry barrier carries every rank's buffer
+// length (LengthMismatch) and an exit barrier guarantees no peer still reads
+// a buffer when the call returns. Waits are bounded by a globaltimer watchdog
+// (NotExposed). No flag is ever reset: epochs only grow.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "md_common.cuh"
+
+namespace md {
+
+constexpr int kMaxSegs = 4096;        // per color
+constexpr int kArThreads = 512;
+// float4 per thread per source per pass: 512 threads x 2 x 16 B keeps >= 16 KB
+// per SM in flight per source (NVLink needs ~5 KB/SM at 775 GB/s x 1 us)
+constexpr int kUnroll = 2;
+
+struct Ctrl {
+  unsigned long long arrive_len[MD_MAX_RANKS];  // from peer r: n | n_workers << 56
+  uint32_t arrive_epoch[MD_MAX_RANKS];
+  uint32_t done_epoch[MD_MAX_RANKS];
+  uint32_t pad0[32 - 2 * MD_MAX_RANKS % 32];
+  uint32_t queue_head;   // local work queue counter
+  uint32_t pad1[31];
+  uint32_t finished;     // CTAs of this rank done with the current call
+  uint32_t abort_flag;   // set by any CTA of this rank that bailed out
+  uint32_t epoch;        // calls completed by this rank (device-side counter)
+  uint32_t pad2[29];
+  uint32_t up[MD_MAX_COLORS][MD_MAX_RANKS + 1][kMaxSegs];
+  uint32_t down[MD_MAX_COLORS][kMaxSegs];
+};
+
+struct Task {
+  int32_t type;  // 0 = UP (fold), 1 = DOWN (copy final from parent)
+  int32_t color;
+  int32_t stage;
+  int32_t n_fold;
+  int32_t parent;   // -1 at the root
+  int32_t my_slot;  // UP, non-root: my position in the parent's fold list
+  int32_t n_down;   // ranks that need my final value (children)
+  int32_t is_leaf;
+  int32_t fold_src[MD_MAX_RANKS + 1];
+  int32_t fold_leaf[MD_MAX_RANKS + 1];
+  int32_t down[MD_MAX_RANKS];
+};
+
+struct RankPlan {
+  int32_t n_tasks;
+  int32_t pad[3];
+  Task t[2 * MD_MAX_COLORS];
+};
+
+struct ViewArgs {
+  float* buf;
+  const float* peer[MD_MAX_RANKS];
+  Ctrl* ctrl;
+  Ctrl* peer_ctrl[MD_MAX_RANKS];
+  const float* workers[MD_MAX_WORKERS];
+  float* w;
+  float* mom;
+  int32_t* err;  // host-mapped: [code, detail]
+  int32_t rank;
+  uint32_t epoch;
+};
+
+struct AllreduceArgs {
+  const RankPlan* plan;
+  int64_t n;
+  int64_t seg;
+  int64_t update_len;
+  unsigned long long timeout_ns;
+  int32_t n_ranks, k, n_views, ctas_per_view;
+  int32_t max_nseg, n_workers;
+  int32_t has_update, vec_ok;
+  float c, mu, wd_b;
+  ViewArgs v[MD_MAX_RANKS];
+};
+
+}  // namespace md
+
+struct md_comm {
+  int32_t rank, n_ranks, device;
+  md::Ctrl* ctrl;
+  md::Ctrl* peer_ctrl[MD_MAX_RANKS];
+  int32_t* err_host;  // pinned, mapped
+  int32_t* err_dev;
+  uint32_t epoch;
+  double timeout_s;
+};
+
+struct md_plan {
+  int32_t n_ranks, k, device;
+  md::RankPlan* dev;                   // n_ranks entries
+  std::vector<md::RankPlan> host;
+};
+
+namespace md {
+
+// ---- chunk / segment geometry (make_chunk_plan, topology.py:103-120) --------
+__host__ __device__ __forceinline__ void chunk_of(int64_t n, int k, int c, int64_t* start,
+                                                  int64_t* len) {
+  int64_t base = n / k, extra = n % k;
+  *start = c * base + (c < extra ? c : extra);
+  *len = base + (c < extra ? 1 : 0);
+}
+__host__ __device__ __forceinline__ int64_t nseg_of(int64_t start, int64_t len, int64_t seg) {
+  if (len <= 0) return 0;
+  int64_t a = start & ~int64_t(3);
+  return (start + len - a + seg - 1) / seg;
+}
+
+// ---- device helpers -----------------------------------------------------------
+__device__ __forceinline__ void raise_err(const ViewArgs& v, int code, int detail) {
+  volatile int32_t* e = v.err;
+  if (e[0] == 0) {
+    e[1] = detail;
+    e[0] = code;
+  }
+  atomicExch(&v.ctrl->abort_flag, 1u);
+}
+
+// Thread 0 spins until *flag >= epoch. Returns false on timeout/abort.
+__device__ bool wait_flag(const ViewArgs& v, const uint32_t* flag, uint32_t epoch,
+                          unsigned long long timeout_ns, int detail) {
+  if (epoch_ge(ld_acquire_sys(flag), epoch)) return true;
+  uint64_t t0 = globaltimer_ns();
+  uint32_t spins = 0;
+  while (true) {
+    if (epoch_ge(ld_acquire_sys(flag), epoch)) return true;
+    if ((++spins & 255) == 0) {
+      if (*reinterpret_cast<volatile uint32_t*>(&v.ctrl->abort_flag)) return false;
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        raise_err(v, MD_ERR_TIMEOUT, detail);
+        return false;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+template <bool kVec>
+struct Elem;
+template <>
+struct Elem<true> {
+  using T = float4;
+  static __device__ __forceinline__ T ld(const float* p, int64_t i) {
+    return *reinterpret_cast<const float4*>(p + i);
+  }
+  static __device__ __forceinline__ T ld_stream(const float* p, int64_t i) {
+    return __ldcs(reinterpret_cast<const float4*>(p + i));
+  }
+  static __device__ __forceinline__ void st(float* p, int64_t i, T x) {
+    *reinterpret_cast<float4*>(p + i) = x;
+  }
+  static __device__ __forceinline__ T add(T a, T b) { return add4(a, b); }
+  static constexpr int W = 4;
+};
+template <>
+struct Elem<false> {
+  using T = float;
+  static __device__ __forceinline__ T ld(const float* p, int64_t i) { return p[i]; }
+  static __device__ __forceinline__ T ld_stream(const float* p, int64_t i) { return p[i]; }
+  static __device__ __forceinline__ void st(float* p, int64_t i, T x) { p[i] = x; }
+  static __device__ __forceinline__ T add(T a, T b) { return __fadd_rn(a, b); }
+  static constexpr int W = 1;
+};
+
+// ---- SGD epilogue -------------------------------------------------------------
+// kEpi: 0 none, 1 plain SGD, 2 + weight decay, 3 + momentum, 4 momentum + wd.
+// A compile-time variant per item keeps the unrolled loops branch-free.
+template <int kEpi>
+__device__ __forceinline__ void sgd_elem(float& w, float g, float& m, const AllreduceArgs& a) {
+  if constexpr (kEpi == 1) sgd1<false, false>(w, g, &m, a.c, a.mu, a.wd_b);
+  if constexpr (kEpi == 2) sgd1<true, false>(w, g, &m, a.c, a.mu, a.wd_b);
+  if constexpr (kEpi == 3) sgd1<false, true>(w, g, &m, a.c, a.mu, a.wd_b);
+  if constexpr (kEpi == 4) sgd1<true, true>(w, g, &m, a.c, a.mu, a.wd_b);
+}
+
+template <int kEpi>
+__device__ __forceinline__ void epi_scalar(const AllreduceArgs& a, const ViewArgs& v, int64_t i,
+                                           float g) {
+  if constexpr (kEpi == 0) return;
+  if (i >= a.update_len) return;
+  constexpr bool kMom = kEpi >= 3;
+  float w = v.w[i];
+  float m = kMom ? v.mom[i] : 0.f;
+  sgd_elem<kEpi>(w, g, m, a);
+  v.w[i] = w;
+  if (kMom) v.mom[i] = m;
+}
+
+// One unrolled batch of a thread (elements b + u*nthr*W): all W/momentum loads
+// are issued before any store, so 2*kUnroll 16-byte loads are in flight.
+template <bool kVec, int kEpi>
+__device__ __forceinline__ void epi_batch(const AllreduceArgs& a, const ViewArgs& v, int64_t b,
+                                          int64_t hi, int nthr,
+                                          const typename Elem<kVec>::T (&g)[kUnroll]) {
+  if constexpr (kEpi == 0) return;
+  constexpr bool kMom = kEpi >= 3;
+  if constexpr (!kVec) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      int64_t i = b + static_cast<int64_t>(u) * nthr;
+      if (i < hi) epi_scalar<kEpi>(a, v, i, g[u]);
+    }
+  } else {
+    const int64_t last = b + static_cast<int64_t>(kUnroll - 1) * nthr * 4;
+    if (last + 3 >= a.update_len || last >= hi) {  // ragged batch: element by element
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t i = b + static_cast<int64_t>(u) * nthr * 4;
+        if (i < hi) {
+          epi_scalar<kEpi>(a, v, i, g[u].x);
+          epi_scalar<kEpi>(a, v, i + 1, g[u].y);
+          epi_scalar<kEpi>(a, v, i + 2, g[u].z);
+          epi_scalar<kEpi>(a, v, i + 3, g[u].w);
+        }
+      }
+      return;
+    }
+    float4 w[kUnroll], m[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = b + static_cast<int64_t>(u) * nthr * 4;
+      w[u] = __ldcs(reinterpret_cast<const float4*>(v.w + i));
+      if constexpr (kMom) m[u] = __ldcs(reinterpret_cast<const float4*>(v.mom + i));
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      sgd_elem<kEpi>(w[u].x, g[u].x, m[u].x, a);
+      sgd_elem<kEpi>(w[u].y, g[u].y, m[u].y, a);
+      sgd_elem<kEpi>(w[u].z, g[u].z, m[u].z, a);
+      sgd_elem<kEpi>(w[u].w, g[u].w, m[u].w, a);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t i = b + static_cast<int64_t>(u) * nthr * 4;
+      __stcs(reinterpret_cast<float4*>(v.w + i), w[u]);
+      if constexpr (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m[u]);
+    }
+  }
+}
+
+// Own value at element i: the buffer, or the worker fold (worker order).
+template <bool kVec>
+__device__ __forceinline__ typename Elem<kVec>::T own_value(const AllreduceArgs& a,
+                                                            const ViewArgs& v, int64_t i) {
+  using E = Elem<kVec>;
+  if (a.n_workers == 0) return E::ld(v.buf, i);
+  typename E::T x = E::ld_stream(v.workers[0], i);
+  for (int j = 1; j < a.n_workers; ++j) x = E::add(x, E::ld_stream(v.workers[j], i));
+  return x;
+}
+
+// Process elements [lo, hi) (all W-aligned when kVec) of one item. kEpi is
+// the epilogue variant where this item makes a segment final, 0 elsewhere.
+template <bool kVec, int kEpi>
+__device__ __forceinline__ void item_data(const AllreduceArgs& a, const ViewArgs& v, const Task& t,
+                                          int64_t lo, int64_t hi, int tid, int nthr) {
+  using E = Elem<kVec>;
+  constexpr int W = E::W;
+  const int64_t step = static_cast<int64_t>(nthr) * W * kUnroll;
+  if (t.type == 1) {  // DOWN: copy the parent's final value
+    const float* src = v.peer[t.parent];
+    for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
+      typename E::T x[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+        if (i < hi) x[u] = E::ld(src, i);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+        if (i < hi) E::st(v.buf, i, x[u]);
+      }
+      epi_batch<kVec, kEpi>(a, v, b, hi, nthr, x);
+    }
+    return;
+  }
+  if (t.n_fold == 1 && a.n_workers == 0) {  // lone rank: the sum is the buffer itself
+    if constexpr (kEpi != 0) {
+      for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
+        typename E::T g[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+          if (i < hi) g[u] = E::ld_stream(v.buf, i);
+        }
+        epi_batch<kVec, kEpi>(a, v, b, hi, nthr, g);
+      }
+    }
+    return;
+  }
+  // UP: fold own value and children in the plan's order
+  for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
+    typename E::T acc[kUnroll];
+    for (int j = 0; j < t.n_fold; ++j) {
+      const int src_rank = t.fold_src[j];
+      typename E::T x[kUnroll];
+      if (src_rank == v.rank) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+          if (i < hi) x[u] = own_value<kVec>(a, v, i);
+        }
+      } else {
+        const float* src = v.peer[src_rank];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+          if (i < hi) x[u] = E::ld(src, i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) acc[u] = (j == 0) ? x[u] : E::add(acc[u], x[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+      if (i < hi) E::st(v.buf, i, acc[u]);
+    }
+    epi_batch<kVec, kEpi>(a, v, b, hi, nthr, acc);
+  }
+}
+
+// The kernel is instantiated per epilogue variant (chosen on the host for the
+// whole call); items that do not make a segment final run variant 0.
+template <bool kVec, int kEpi>
+__device__ __forceinline__ void item_dispatch(const AllreduceArgs& a, const ViewArgs& v,
+                                              const Task& t, bool final_here, int64_t lo,
+                                              int64_t hi, int tid, int nthr) {
+  if (kEpi != 0 && final_here) item_data<kVec, kEpi>(a, v, t, lo, hi, tid, nthr);
+  else item_data<kVec, 0>(a, v, t, lo, hi, tid, nthr);
+}
+
+// Entry barrier + length agreement. Returns false if this view must skip work.
+__device__ bool entry_barrier(const AllreduceArgs& a, const ViewArgs& v, int local_cta,
+                              uint32_t epoch) {
+  const int tid = threadIdx.x;
+  const unsigned long long mylen =
+      static_cast<unsigned long long>(a.n) | (static_cast<unsigned long long>(a.n_workers) << 56);
+  if (local_cta == 0 && tid < a.n_ranks && tid != v.rank) {
+    Ctrl* pc = v.peer_ctrl[tid];
+    st_relaxed_sys64(reinterpret_cast<uint64_t*>(&pc->arrive_len[v.rank]), mylen);
+    __threadfence_system();
+    st_release_sys(&pc->arrive_epoch[v.rank], epoch);
+  }
+  __shared__ int s_ok;
+  if (tid == 0) {
+    int ok = 1;
+    for (int r = 0; r < a.n_ranks && ok; ++r) {
+      if (r == v.rank) continue;
+      if (!wait_flag(v, &v.ctrl->arrive_epoch[r], epoch, a.timeout_ns, 1000 + r)) {
+        ok = 0;
+        break;
+      }
+      unsigned long long len =
+          ld_relaxed_sys64(reinterpret_cast<const uint64_t*>(&v.ctrl->arrive_len[r]));
+      if (len != mylen) {
+        // every rank sees the same table, so every rank reports the mismatch
+        if (local_cta == 0) raise_err(v, MD_ERR_LENGTH_MISMATCH, r);
+        ok = 0;
+      }
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+__device__ void exit_barrier(const AllreduceArgs& a, const ViewArgs& v, uint32_t epoch) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t prev = atomicAdd(&v.ctrl->finished, 1u);
+    s_last = (prev == static_cast<uint32_t>(a.ctas_per_view - 1));
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // last CTA of this rank: nobody here reads peer memory any more
+  const int tid = threadIdx.x;
+  if (tid < a.n_ranks && tid != v.rank) {
+    __threadfence_system();
+    st_release_sys(&v.peer_ctrl[tid]->done_epoch[v.rank], epoch);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int r = 0; r < a.n_ranks; ++r) {
+      if (r == v.rank) continue;
+      // abort does not short-circuit here: peers still need our done flag,
+      // and theirs bound the time anybody may still read our buffer
+      uint64_t t0 = globaltimer_ns();
+      while (!epoch_ge(ld_acquire_sys(&v.ctrl->done_epoch[r]), epoch)) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          raise_err(v, MD_ERR_TIMEOUT, 2000 + r);
+          break;
+        }
+        __nanosleep(32);
+      }
+    }
+    v.ctrl->queue_head = 0;
+    v.ctrl->finished = 0;
+    v.ctrl->abort_flag = 0;
+    v.ctrl->epoch = epoch;
+    __threadfence();
+  }
+}
+
+template <int kEpi>
+__global__ void __launch_bounds__(kArThreads, 1)
+    allreduce_kernel(const __grid_constant__ AllreduceArgs a) {
+  const int view = blockIdx.x / a.ctas_per_view;
+  const int local_cta = blockIdx.x % a.ctas_per_view;
+  const ViewArgs& v = a.v[view];
+  const RankPlan& rp = a.plan[v.rank];
+  const int tid = threadIdx.x, nthr = blockDim.x;
+
+  // the epoch lives in the control block (device side), so a captured CUDA
+  // graph can replay this launch: every call bumps it exactly once
+  __shared__ uint32_t s_epoch;
+  if (tid == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  bool ok = entry_barrier(a, v, local_cta, epoch);
+  const int n_tasks = rp.n_tasks;
+  const int64_t n_items = static_cast<int64_t>(a.max_nseg) * n_tasks;
+  __shared__ int64_t s_item;
+  __shared__ int s_go;
+
+  while (ok) {
+    if (tid == 0) {
+      s_item = atomicAdd(&v.ctrl->queue_head, 1u);
+      if (*reinterpret_cast<volatile uint32_t*>(&v.ctrl->abort_flag)) s_item = n_items;
+    }
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= n_items) break;
+    const int s = static_cast<int>(item / n_tasks);
+    const Task& t = rp.t[item % n_tasks];
+    int64_t cstart, clen;
+    chunk_of(a.n, a.k, t.color, &cstart, &clen);
+    if (s >= nseg_of(cstart, clen, a.seg)) {
+      __syncthreads();
+      continue;
+    }
+    if (t.type == 0 && t.is_leaf && a.n_workers == 0) {  // leaf data ready at entry
+      __syncthreads();
+      continue;
+    }
+    const int64_t A = cstart & ~int64_t(3);
+    const int64_t lo = max(cstart, A + static_cast<int64_t>(s) * a.seg);
+    const int64_t hi = min(cstart + clen, A + static_cast<int64_t>(s + 1) * a.seg);
+
+    // ---- wait for producers
+    if (tid == 0) {
+      int go = 1;
+      if (t.type == 1) {
+        go = wait_flag(v, &v.ctrl->down[t.color][s], epoch, a.timeout_ns, 3000 + t.color);
+      } else {
+        for (int j = 0; j < t.n_fold && go; ++j) {
+          if (t.fold_src[j] == v.rank) continue;
+          if (t.fold_leaf[j] && a.n_workers == 0) continue;
+          go = wait_flag(v, &v.ctrl->up[t.color][j][s], epoch, a.timeout_ns, 4000 + t.color);
+        }
+      }
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) break;
+
+    // ---- data
+    const bool final_here = (t.type == 1) || (t.parent < 0);
+    const int64_t vlo = min(hi, (lo + 3) & ~int64_t(3));
+    const int64_t vhi = max(vlo, hi & ~int64_t(3));
+    if (a.vec_ok) {
+      item_dispatch<true, kEpi>(a, v, t, final_here, vlo, vhi, tid, nthr);
+      if (tid < 8) {  // <= 3 head + <= 3 tail scalars
+        int64_t i = (tid < 4) ? lo + tid : vhi + (tid - 4);
+        bool mine = (tid < 4) ? (i < vlo) : (i < hi);
+        if (mine) item_dispatch<false, kEpi>(a, v, t, final_here, i, i + 1, 0, 1);
+      }
+    } else {
+      item_dispatch<false, kEpi>(a, v, t, final_here, lo, hi, tid, nthr);
+    }
+    __syncthreads();
+
+    // ---- publish
+    if (t.type == 0 && t.parent >= 0) {
+      if (tid == 0) {
+        __threadfence_system();
+        st_release_sys(&v.peer_ctrl[t.parent]->up[t.color][t.my_slot][s], epoch);
+      }
+    } else if (final_here) {
+      if (tid < t.n_down) {
+        __threadfence_system();
+        st_release_sys(&v.peer_ctrl[t.down[tid]]->down[t.color][s], epoch);
+      }
+    }
+  }
+  exit_barrier(a, v, epoch);
+}
+
+// ---- plan construction (host) ------------------------------------------------
+static int build_rank_plans(int n, int k, const int32_t* parent, const int32_t* child_ptr,
+                            const int32_t* child_idx, const int32_t* self_pos,
+                            std::vector<RankPlan>* out) {
+  out->assign(n, RankPlan{});
+  for (int c = 0; c < k; ++c) {
+    const int32_t* par = parent + c * n;
+    int root = -1;
+    for (int r = 0; r < n; ++r) {
+      if (par[r] < -1 || par[r] >= n || par[r] == r) {
+        set_error("color %d: bad parent %d of rank %d", c, par[r], r);
+        return MD_ERR_INVALID_CONFIG;
+      }
+      if (par[r] == -1) {
+        if (root >= 0) {
+          set_error("color %d has two roots (%d, %d)", c, root, r);
+          return MD_ERR_INVALID_CONFIG;
+        }
+        root = r;
+      }
+    }
+    if (root < 0) {
+      set_error("color %d has no root", c);
+      return MD_ERR_INVALID_CONFIG;
+    }
+    auto kids = [&](int r, int* cnt) {
+      int row = c * n + r;
+      *cnt = child_ptr[row + 1] - child_ptr[row];
+      return child_idx + child_ptr[row];
+    };
+    // consistency + acyclicity: depth via parent chain (<= n steps)
+    std::vector<int> depth(n, -1), height(n, 0);
+    for (int r = 0; r < n; ++r) {
+      int d = 0, cur = r;
+      while (par[cur] >= 0 && d <= n) {
+        cur = par[cur];
+        ++d;
+      }
+      if (d > n || cur != root) {
+        set_error("color %d: cycle reachable from rank %d", c, r);
+        return MD_ERR_INVALID_CONFIG;
+      }
+      depth[r] = d;
+      int cnt;
+      const int32_t* ch = kids(r, &cnt);
+      if (cnt < 0 || cnt > MD_MAX_RANKS) {
+        set_error("color %d: rank %d has %d children", c, r, cnt);
+        return MD_ERR_INVALID_CONFIG;
+      }
+      for (int j = 0; j < cnt; ++j) {
+        if (ch[j] < 0 || ch[j] >= n || par[ch[j]] != r) {
+          set_error("color %d: child %d of %d disagrees with parent map", c, ch[j], r);
+          return MD_ERR_INVALID_CONFIG;
+        }
+      }
+    }
+    int total_children = 0;
+    for (int r = 0; r < n; ++r) {
+      int cnt;
+      kids(r, &cnt);
+      total_children += cnt;
+    }
+    if (total_children != n - 1) {
+      set_error("color %d: children lists cover %d ranks, expected %d", c, total_children, n - 1);
+      return MD_ERR_INVALID_CONFIG;
+    }
+    // heights, deepest first
+    std::vector<int> order(n);
+    for (int r = 0; r < n; ++r) order[r] = r;
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return depth[x] > depth[y]; });
+    for (int r : order)
+      if (par[r] >= 0) height[par[r]] = std::max(height[par[r]], height[r] + 1);
+    const int H = height[root];
+
+    auto fold_pos = [&](int r) { return self_pos ? self_pos[c * n + r] : 0; };
+    for (int r = 0; r < n; ++r) {
+      RankPlan& rp = (*out)[r];
+      int cnt;
+      const int32_t* ch = kids(r, &cnt);
+      int sp = fold_pos(r);
+      if (sp < 0 || sp > cnt) {
+        set_error("color %d: self position %d out of range for rank %d", c, sp, r);
+        return MD_ERR_INVALID_CONFIG;
+      }
+      Task up{};
+      up.type = 0;
+      up.color = c;
+      up.stage = height[r];
+      up.parent = par[r];
+      up.is_leaf = cnt == 0;
+      up.n_fold = cnt + 1;
+      for (int j = 0, q = 0; j <= cnt; ++j) {
+        if (j == sp) {
+          up.fold_src[j] = r;
+          up.fold_leaf[j] = 0;
+        } else {
+          int chr = ch[q++];
+          up.fold_src[j] = chr;
+          int gc;
+          kids(chr, &gc);
+          up.fold_leaf[j] = gc == 0;
+        }
+      }
+      if (par[r] >= 0) {
+        int pcnt;
+        const int32_t* pch = kids(par[r], &pcnt);
+        int ci = 0;
+        while (ci < pcnt && pch[ci] != r) ++ci;
+        int psp = fold_pos(par[r]);
+        up.my_slot = ci >= psp ? ci + 1 : ci;
+      } else {
+        up.n_down = cnt;
+        for (int j = 0; j < cnt; ++j) up.down[j] = ch[j];
+      }
+      rp.t[rp.n_tasks++] = up;
+      if (par[r] >= 0) {
+        Task dn{};
+        dn.type = 1;
+        dn.color = c;
+        dn.stage = H + depth[r];
+        dn.parent = par[r];
+        dn.n_down = cnt;
+        for (int j = 0; j < cnt; ++j) dn.down[j] = ch[j];
+        rp.t[rp.n_tasks++] = dn;
+      }
+    }
+  }
+  for (auto& rp : *out)
+    std::stable_sort(rp.t, rp.t + rp.n_tasks,
+                     [](const Task& x, const Task& y) { return x.stage < y.stage; });
+  return MD_OK;
+}
+
+}  // namespace md
+
+using namespace md;
+
+extern "C" {
+
+int md_device_count(int* n) {
+  MD_CUDA_TRY(cudaGetDeviceCount(n));
+  return MD_OK;
+}
+
+int md_enable_peer_access(int dev, int peer) {
+  if (dev == peer) return MD_OK;
+  int prev;
+  MD_CUDA_TRY(cudaGetDevice(&prev));
+  MD_CUDA_TRY(cudaSetDevice(dev));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    e = cudaSuccess;
+  }
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    set_error("cudaDeviceEnablePeerAccess(%d -> %d): %s", dev, peer, cudaGetErrorString(e));
+    return MD_ERR_CUDA;
+  }
+  return MD_OK;
+}
+
+typedef int (*PFN_getAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+int md_mem_export(const void* ptr, unsigned char handle[MD_IPC_HANDLE_BYTES], uint64_t* offset) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    MD_CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q));
+    if (!p) {
+      set_error("cuMemGetAddressRange unavailable");
+      return MD_ERR_CUDA;
+    }
+    fn = reinterpret_cast<PFN_getAddressRange>(p);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  int rc = fn(&base, &size, reinterpret_cast<unsigned long long>(ptr));
+  if (rc != 0) {
+    set_error("cuMemGetAddressRange failed (%d)", rc);
+    return MD_ERR_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  MD_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == MD_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *offset = reinterpret_cast<unsigned long long>(ptr) - base;
+  return MD_OK;
+}
+
+int md_mem_import(const unsigned char handle[MD_IPC_HANDLE_BYTES], void** base) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  MD_CUDA_TRY(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  return MD_OK;
+}
+
+int md_mem_close(void* base) {
+  MD_CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return MD_OK;
+}
+
+int md_comm_create(int32_t rank, int32_t n_ranks, int32_t device, md_comm_t** out) {
+  if (n_ranks < 1 || n_ranks > MD_MAX_RANKS || rank < 0 || rank >= n_ranks) {
+    set_error("rank %d of %d unsupported (max %d ranks)", rank, n_ranks, MD_MAX_RANKS);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  int prev;
+  MD_CUDA_TRY(cudaGetDevice(&prev));
+  MD_CUDA_TRY(cudaSetDevice(device));
+  md_comm* c = new md_comm();
+  c->rank = rank;
+  c->n_ranks = n_ranks;
+  c->device = device;
+  c->epoch = 0;
+  c->timeout_s = 30.0;
+  cudaError_t e = cudaMalloc(&c->ctrl, sizeof(Ctrl));
+  if (e == cudaSuccess) e = cudaMemset(c->ctrl, 0, sizeof(Ctrl));
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->err_host, 2 * sizeof(int32_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    c->err_host[0] = c->err_host[1] = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    set_error("md_comm_create: %s", cudaGetErrorString(e));
+    delete c;
+    return MD_ERR_CUDA;
+  }
+  for (int r = 0; r < MD_MAX_RANKS; ++r) c->peer_ctrl[r] = nullptr;
+  c->peer_ctrl[rank] = c->ctrl;
+  *out = c;
+  return MD_OK;
+}
+
+int md_comm_destroy(md_comm_t* c) {
+  if (!c) return MD_OK;
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  cudaFree(c->ctrl);
+  cudaFreeHost(c->err_host);
+  cudaSetDevice(prev);
+  delete c;
+  return MD_OK;
+}
+
+int md_comm_ctrl_ptr(md_comm_t* c, void** ctrl) {
+  *ctrl = c->ctrl;
+  return MD_OK;
+}
+
+int md_comm_set_peer_ctrl(md_comm_t* c, void* const* ptrs, int32_t n) {
+  if (n != c->n_ranks) {
+    set_error("expected %d control pointers, got %d", c->n_ranks, n);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  for (int r = 0; r < n; ++r)
+    c->peer_ctrl[r] = (r == c->rank) ? c->ctrl : static_cast<Ctrl*>(ptrs[r]);
+  return MD_OK;
+}
+
+int md_comm_take_error(md_comm_t* c, int32_t* code, int32_t* detail) {
+  volatile int32_t* e = c->err_host;
+  *code = e[0];
+  *detail = e[1];
+  e[0] = 0;
+  e[1] = 0;
+  return MD_OK;
+}
+
+int md_comm_set_timeout(md_comm_t* c, double seconds) {
+  if (!(seconds > 0)) {
+    set_error("timeout must be > 0");
+    return MD_ERR_INVALID_CONFIG;
+  }
+  c->timeout_s = seconds;
+  return MD_OK;
+}
+
+int md_plan_create(int32_t n_ranks, int32_t k, const int32_t* parent, const int32_t* child_ptr,
+                   const int32_t* child_idx, const int32_t* self_pos, int32_t device,
+                   md_plan_t** out) {
+  if (n_ranks < 1 || n_ranks > MD_MAX_RANKS) {
+    set_error("n_ranks %d unsupported (max %d)", n_ranks, MD_MAX_RANKS);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  if (k < 1 || k > MD_MAX_COLORS) {
+    set_error("%d colors unsupported (max %d)", k, MD_MAX_COLORS);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  std::vector<RankPlan> host;
+  int rc = build_rank_plans(n_ranks, k, parent, child_ptr, child_idx, self_pos, &host);
+  if (rc != MD_OK) return rc;
+  int prev;
+  MD_CUDA_TRY(cudaGetDevice(&prev));
+  MD_CUDA_TRY(cudaSetDevice(device));
+  md_plan* p = new md_plan();
+  p->n_ranks = n_ranks;
+  p->k = k;
+  p->device = device;
+  p->host = host;
+  cudaError_t e = cudaMalloc(&p->dev, sizeof(RankPlan) * n_ranks);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->dev, host.data(), sizeof(RankPlan) * n_ranks, cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    set_error("md_plan_create: %s", cudaGetErrorString(e));
+    delete p;
+    return MD_ERR_CUDA;
+  }
+  *out = p;
+  return MD_OK;
+}
+
+int md_plan_destroy(md_plan_t* p) {
+  if (!p) return MD_OK;
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(p->device);
+  cudaFree(p->dev);
+  cudaSetDevice(prev);
+  delete p;
+  return MD_OK;
+}
+
+int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan,
+                 float* const* bufs, int64_t n, const float* const* workers, int32_t n_workers,
+                 float* const* w, float* const* mom, int64_t update_len, float c, float mu,
+                 float wd_b, int64_t seg_elems, int32_t ctas, void* stream) {
+  if (!plan || n_views < 1 || n_views > MD_MAX_RANKS) {
+    set_error("bad plan/view count");
+    return MD_ERR_INVALID_CONFIG;
+  }
+  const int N = plan->n_ranks;
+  if (n < 0) {
+    set_error("negative length");
+    return MD_ERR_INVALID_CONFIG;
+  }
+  if (n_workers < 0 || n_workers > MD_MAX_WORKERS || (n_workers > 0 && !workers)) {
+    set_error("bad worker count %d (max %d)", n_workers, MD_MAX_WORKERS);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  if (seg_elems < 1) {
+    set_error("segment_elems must be >= 1, got %lld", (long long)seg_elems);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  const bool has_update = w != nullptr;
+  if (has_update && (update_len < 0 || update_len > n)) {
+    set_error("update_len %lld outside [0, %lld]", (long long)update_len, (long long)n);
+    return MD_ERR_LENGTH_MISMATCH;
+  }
+  AllreduceArgs a;
+  memset(&a, 0, sizeof(a));
+  a.plan = plan->dev;
+  a.n = n;
+  a.n_ranks = N;
+  a.k = plan->k;
+  a.n_views = n_views;
+  a.n_workers = n_workers;
+  a.has_update = has_update;
+  a.update_len = has_update ? update_len : 0;
+  a.c = c;
+  a.mu = mu;
+  a.wd_b = wd_b;
+  // segment length: multiple of 4 elements, <= kMaxSegs segments per color
+  int64_t maxlen = (n + plan->k - 1) / plan->k;
+  int64_t seg = std::max<int64_t>(4, (seg_elems + 3) & ~int64_t(3));
+  int64_t min_seg = ((maxlen + 3) / kMaxSegs + 4 + 3) & ~int64_t(3);
+  if (seg < min_seg) seg = min_seg;
+  a.seg = seg;
+  int64_t mx = 0;
+  for (int col = 0; col < plan->k; ++col) {
+    int64_t st, ln;
+    chunk_of(n, plan->k, col, &st, &ln);
+    mx = std::max(mx, nseg_of(st, ln, seg));
+  }
+  a.max_nseg = static_cast<int32_t>(mx);
+  uintptr_t bits = 0;
+  double timeout = 30.0;
+  for (int vi = 0; vi < n_views; ++vi) {
+    md_comm* cm = comms[vi];
+    if (!cm || cm->n_ranks != N) {
+      set_error("communicator/plan world size mismatch (%d vs %d)", cm ? cm->n_ranks : -1, N);
+      return MD_ERR_INVALID_CONFIG;
+    }
+    ViewArgs& v = a.v[vi];
+    v.rank = cm->rank;
+    v.ctrl = cm->ctrl;
+    for (int r = 0; r < N; ++r) {
+      if (!cm->peer_ctrl[r]) {
+        set_error("rank %d: control block of peer %d not installed", cm->rank, r);
+        return MD_ERR_INVALID_CONFIG;
+      }
+      v.peer_ctrl[r] = cm->peer_ctrl[r];
+      v.peer[r] = bufs[vi * N + r];
+      bits |= reinterpret_cast<uintptr_t>(v.peer[r]);
+    }
+    v.buf = bufs[vi * N + cm->rank];
+    for (int j = 0; j < n_workers; ++j) {
+      v.workers[j] = workers[vi * n_workers + j];
+      bits |= reinterpret_cast<uintptr_t>(v.workers[j]);
+    }
+    if (has_update) {
+      v.w = w[vi];
+      v.mom = (mom && mu != 0.f) ? mom[vi] : nullptr;
+      bits |= reinterpret_cast<uintptr_t>(v.w) | reinterpret_cast<uintptr_t>(v.mom);
+    }
+    v.err = cm->err_dev;
+    ++cm->epoch;
+    timeout = std::min(timeout, cm->timeout_s);
+  }
+  a.vec_ok = (bits & 15) == 0;
+  a.timeout_ns = static_cast<unsigned long long>(timeout * 1e9);
+
+  int dev;
+  MD_CUDA_TRY(cudaGetDevice(&dev));
+  int per_sm = 0;
+  int epi = 0;
+  if (has_update) epi = (a.v[0].mom ? 3 : 1) + (wd_b != 0.f ? 1 : 0);
+  const void* kern = nullptr;
+  switch (epi) {
+    case 1: kern = reinterpret_cast<const void*>(allreduce_kernel<1>); break;
+    case 2: kern = reinterpret_cast<const void*>(allreduce_kernel<2>); break;
+    case 3: kern = reinterpret_cast<const void*>(allreduce_kernel<3>); break;
+    case 4: kern = reinterpret_cast<const void*>(allreduce_kernel<4>); break;
+    default: kern = reinterpret_cast<const void*>(allreduce_kernel<0>); break;
+  }
+  MD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArThreads, 0));
+  int resident = per_sm * sm_count(dev);
+  if (ctas <= 0) ctas = resident / n_views;
+  ctas = std::min(ctas, resident / n_views);
+  if (ctas < 1) {
+    set_error("%d views do not fit co-resident on device %d", n_views, dev);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  a.ctas_per_view = ctas;
+  void* args[] = {&a};
+  // cooperative launch: every CTA (of every emulated rank) co-resident, so
+  // flag waits between CTAs can never deadlock on scheduling
+  MD_CUDA_TRY(cudaLaunchCooperativeKernel(kern,
+                                          dim3(ctas * n_views), dim3(kArThreads), args, 0,
+                                          as_stream(stream)));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return MD_OK;
+}
+
+}  // extern "C"

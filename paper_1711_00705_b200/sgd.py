@@ -1,0 +1,280 @@
+"""Synchronous data-parallel SGD step ("data-parallel table") on B200.
+
+API of /root/reference/pkg/src/minidist/sgd.py around its hot path:
+``train_step`` (:382-426) samples each worker's sub-batch from the DIMD
+shard (:290-314), obtains per-worker gradient sums with the loss and the
+correct count in two tail slots (:335-353), sums them across ranks, applies
+``W -= fl32(lr/B) * g`` (:416) and certifies the replicas (:356-379).
+
+On B200 the fold of the worker buffers (gradient accumulation), the
+multicolor allreduce and the weight update are ONE kernel launch
+(collectives.run_fold with ``workers`` + ``update``); the replica check is a
+device digest compared through the host channel.
+
+The model's forward/backward is outside the hot path (the reference uses a
+172-parameter toy MLP as a stand-in for ResNet-50, :147-247): ``train_step``
+takes a ``grad_fn`` producing per-worker gradient buffers. The momentum and
+weight-decay terms are an extension (the reference has plain SGD); with
+``momentum == weight_decay == 0`` the update is bit-identical to
+``sub_scaled_f32(W, g[:p], lr / B)``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from paper_1711_00705_b200 import _lib
+from paper_1711_00705_b200.collectives import (
+    DEFAULT_SEGMENT_ELEMS,
+    GradientBuffer,
+    SgdUpdate,
+    allreduce,
+)
+from paper_1711_00705_b200.dimd import BatchRequest, ShardStore, _mix64, random_batch_device
+from paper_1711_00705_b200.errors import DisjointnessViolation, DivergenceDetected, InvalidConfig
+from paper_1711_00705_b200.topology import build_multicolor_trees, build_ring
+
+SAMPLE_ROLE = int.from_bytes(b"samp", "little")
+SHUFFLE_ROLE = int.from_bytes(b"shuf", "little")
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """Job shape and schedule (sgd.py:58-104); ``momentum`` and
+    ``weight_decay`` extend the reference's plain SGD."""
+
+    n_nodes: int
+    workers_per_node: int
+    per_worker_batch: int
+    epochs: int
+    base_lr: float = 0.1
+    warmup_epochs: int = 5
+    drop_every: int = 30
+    drop_factor: float = 10.0
+    seed: int = 0
+    group_size: int = 1
+    shuffle_every: int = 1
+    sim_compute_per_sample: float = 0.0
+    hidden: int = 8
+    momentum: float = 0.0
+    weight_decay: float = 0.0
+
+    def __post_init__(self):
+        for name in ("n_nodes", "workers_per_node", "per_worker_batch", "epochs"):
+            if getattr(self, name) < 1:
+                raise InvalidConfig(f"{name} must be >= 1, got {getattr(self, name)}")
+        checks = [
+            (self.base_lr > 0, f"base_lr must be > 0, got {self.base_lr}"),
+            (self.warmup_epochs >= 0, f"warmup_epochs must be >= 0, got {self.warmup_epochs}"),
+            (self.drop_every >= 1, f"drop_every must be >= 1, got {self.drop_every}"),
+            (self.drop_factor > 1, f"drop_factor must be > 1, got {self.drop_factor}"),
+            (self.group_size >= 1, f"group_size must be >= 1, got {self.group_size}"),
+            (self.shuffle_every >= 0, f"shuffle_every must be >= 0, got {self.shuffle_every}"),
+            (self.sim_compute_per_sample >= 0, "sim_compute_per_sample must be >= 0"),
+            (self.hidden >= 1, f"hidden must be >= 1, got {self.hidden}"),
+            (0.0 <= self.momentum < 1.0, f"momentum must be in [0, 1), got {self.momentum}"),
+            (self.weight_decay >= 0.0, f"weight_decay must be >= 0, got {self.weight_decay}"),
+        ]
+        for ok, msg in checks:
+            if not ok:
+                raise InvalidConfig(msg)
+
+    @property
+    def effective_batch(self) -> int:
+        return self.n_nodes * self.workers_per_node * self.per_worker_batch
+
+
+@dataclass(frozen=True)
+class LrSchedule:
+    base_lr: float
+    k: int  # per-worker batch
+    n: int  # total workers
+    warmup_epochs: int
+    drop_every: int
+    drop_factor: float
+
+
+def lr_schedule(cfg: TrainConfig) -> LrSchedule:
+    return LrSchedule(cfg.base_lr, cfg.per_worker_batch, cfg.n_nodes * cfg.workers_per_node,
+                      cfg.warmup_epochs, cfg.drop_every, cfg.drop_factor)
+
+
+def lr_at(sched: LrSchedule, epoch: float) -> float:
+    """Warm start (sgd.py:128-141): linear ramp base -> base*k*n/256 over
+    warmup_epochs, then divide by drop_factor every drop_every epochs. The
+    float64 expression order is the reference's, so values are identical."""
+    if epoch < 0:
+        raise InvalidConfig(f"epoch must be >= 0, got {epoch}")
+    target = sched.base_lr * sched.k * sched.n / 256.0
+    if epoch < sched.warmup_epochs:
+        return sched.base_lr + (target - sched.base_lr) * (epoch / sched.warmup_epochs)
+    return target * sched.drop_factor ** (-int((epoch - sched.warmup_epochs) // sched.drop_every))
+
+
+@dataclass
+class DeviceModel:
+    """Replicated flat float32 weights (and momentum) resident on the GPU."""
+
+    weights: torch.Tensor
+    momentum: torch.Tensor | None = None
+
+    @property
+    def n_params(self) -> int:
+        return int(self.weights.numel())
+
+    @classmethod
+    def from_numpy(cls, w: np.ndarray, device, momentum: bool = False) -> DeviceModel:
+        t = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32)).to(device)
+        return cls(t, torch.zeros_like(t) if momentum else None)
+
+
+@dataclass(frozen=True)
+class StepStats:
+    step: int
+    epoch: float
+    lr: float
+    loss: float  # mean loss over the effective batch
+    correct: int
+    samples: int
+    elapsed_s: float = 0.0
+
+    @property
+    def acc(self) -> float:
+        return self.correct / self.samples
+
+
+def sample_node_batch(store: ShardStore, cfg: TrainConfig, rank: int, step: int,
+                      record_bytes: int | None = None):
+    """Per-worker sub-batches carved at the source (sgd.py:290-314): worker j
+    of rank r is global worker r*m+j, keyed _mix64(seed, "samp", worker, step).
+    Returns [(records uint8 [k, L], labels int32 [k], picks int64 [k])]."""
+    out = []
+    for j in range(cfg.workers_per_node):
+        worker = rank * cfg.workers_per_node + j
+        key = _mix64(cfg.seed, SAMPLE_ROLE, worker, step)
+        out.append(random_batch_device(store, BatchRequest(cfg.per_worker_batch, key), record_bytes))
+    return out
+
+
+def node_gradient(worker_bufs: list[torch.Tensor]) -> torch.Tensor:
+    """Fold worker gradient buffers in worker order (sgd.py:335-353) -- the
+    unfused form; train_step fuses this fold into the allreduce prologue."""
+    from paper_1711_00705_b200 import _kernels
+
+    acc = worker_bufs[0].clone()
+    for b in worker_bufs[1:]:
+        _kernels.add_f32(acc, b)
+    return acc
+
+
+def weights_digest(weights: torch.Tensor) -> int:
+    """64-bit device digest of the weight bits (md_digest_f32)."""
+    out = ctypes.c_uint64()
+    _lib.check(
+        _lib.load().md_digest_f32(
+            weights.data_ptr(), weights.numel(), ctypes.byref(out),
+            _lib.stream_ptr(torch.cuda.current_stream(weights.device)),
+        )
+    )
+    return int(out.value)
+
+
+def check_replicas(ep, weights: torch.Tensor, step: int) -> None:
+    """Every rank raises DivergenceDetected unless all replicas' 64-bit device
+    digests agree (sgd.py:356-379; blake2b over host bytes becomes a device
+    reduction, only 8 bytes per rank cross to the host)."""
+    if ep.n_ranks == 1:
+        return
+    digests = ep.all_gather(weights_digest(weights))
+    if any(d != digests[0] for d in digests):
+        raise DivergenceDetected(
+            f"step {step}: replica weight digests differ: " + ", ".join(f"{d:016x}" for d in digests)
+        )
+
+
+def comm_plan(n_ranks: int, algo: str):
+    """Widest color count the rank count supports (sgd.py:453-467)."""
+    tree_set = ring = None
+    if n_ranks > 1:
+        if algo == "multicolor":
+            for k in (4, 2, 1):
+                try:
+                    tree_set = build_multicolor_trees(n_ranks, k=k)
+                    break
+                except (InvalidConfig, DisjointnessViolation):
+                    continue
+        elif algo == "ring":
+            ring = build_ring(n_ranks)
+    return tree_set, ring
+
+
+class StepBuffers:
+    """Per-rank scratch of a training job: the peer-registered gradient
+    buffer (p + 2 floats) and the per-worker gradient buffers."""
+
+    def __init__(self, ep, n_params: int, workers: int):
+        self.grad = GradientBuffer.alloc(n_params + 2, ep)
+        dev = ep.torch_device
+        self.workers = [torch.zeros(n_params + 2, dtype=torch.float32, device=dev)
+                        for _ in range(workers)]
+
+
+def train_step(
+    ep,
+    model: DeviceModel,
+    cfg: TrainConfig,
+    store: ShardStore,
+    algo: str = "multicolor",
+    *,
+    step: int = 0,
+    epoch: float = 0.0,
+    tree_set=None,
+    ring=None,
+    grad_fn=None,
+    buffers: StepBuffers | None = None,
+    record_bytes: int | None = None,
+    verify_replicas: bool = True,
+    segment_elems: int = DEFAULT_SEGMENT_ELEMS,
+    sync: bool = True,
+):
+    """One synchronous step: sample, [fold + allreduce + update] fused, check.
+
+    ``grad_fn(model, batches, worker_bufs)`` writes each worker's summed
+    gradient and its (loss sum, correct count) tail into ``worker_bufs[j]``
+    (p + 2 floats). With ``sync=False`` nothing waits on the device and the
+    returned stats are None (the bench's device-resident loop)."""
+    if ep.n_ranks != cfg.n_nodes:
+        raise InvalidConfig(f"config says {cfg.n_nodes} nodes, running {ep.n_ranks}")
+    if grad_fn is None:
+        raise InvalidConfig("train_step needs a grad_fn (the model is outside the hot path)")
+    lr = lr_at(lr_schedule(cfg), epoch)
+    p = model.n_params
+    if buffers is None:
+        buffers = StepBuffers(ep, p, cfg.workers_per_node)
+    batches = sample_node_batch(store, cfg, ep.rank, step, record_bytes)
+    grad_fn(model, batches, buffers.workers)
+    b = cfg.effective_batch
+    upd = SgdUpdate(
+        weights=model.weights,
+        c=lr / b,
+        momentum=model.momentum,
+        mu=cfg.momentum,
+        wd_b=cfg.weight_decay * b,
+        update_len=p,
+    )
+    allreduce(
+        ep, buffers.grad, algo, tree_set=tree_set, ring=ring, segment_elems=segment_elems,
+        workers=buffers.workers, update=upd, check=sync,
+    )
+    if not sync:
+        return model, None
+    if verify_replicas:
+        check_replicas(ep, model.weights, step)
+    tail = buffers.grad.data[p : p + 2].cpu().numpy()
+    stats = StepStats(step=step, epoch=epoch, lr=lr, loss=float(tail[0]) / b,
+                      correct=int(tail[1]), samples=b)
+    return model, stats

@@ -1,0 +1,225 @@
+"""Allreduce parity on the GPU: every golden case of the reference, bitwise.
+
+Ranks are emulated on one GPU (run_ranks(..., emulate=True): one cooperative
+launch serves all ranks) so this runs on a 1-GPU box; the multigpu tests at
+the bottom repeat the cases with one GPU per rank over NVLink.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1711_00705_b200 import (
+    GradientBuffer,
+    SgdUpdate,
+    allreduce,
+    allreduce_multicolor,
+    build_multicolor_trees,
+    build_ring,
+    errors,
+    run_ranks,
+)
+from tests.conftest import need_gpus
+from tests.test_oracle import GOLD_MC
+
+pytestmark = pytest.mark.gpu
+
+
+def run(n, arrays, algo, emulate=True, **kw):
+    def prog(ep):
+        buf = GradientBuffer(torch.from_numpy(arrays[ep.rank].copy()).to(ep.torch_device))
+        return allreduce(ep, buf, algo, **kw).data.cpu().numpy()
+
+    return run_ranks(n, "cuda", prog, emulate=emulate).results
+
+
+@pytest.mark.parametrize("n,L,k,arity", GOLD_MC)
+@pytest.mark.parametrize("seg", [64, 16384])
+def test_multicolor_matches_reference(golden, n, L, k, arity, seg):
+    inp = golden[f"mc_{n}_{L}_{k}_{arity}_in"]
+    want = golden[f"mc_{n}_{L}_{k}_{arity}_out"]
+    ts = build_multicolor_trees(n, k, arity)
+    for r in run(n, list(inp), "multicolor", tree_set=ts, segment_elems=seg):
+        assert np.array_equal(r, want)
+
+
+@pytest.mark.parametrize("n,L", [(8, 1000), (5, 333), (2, 4), (4, 4099)])
+def test_ring_matches_reference(golden, n, L):
+    out = run(n, list(golden[f"ring_{n}_{L}_in"]), "ring", ring=build_ring(n), segment_elems=100)
+    for r in out:
+        assert np.array_equal(r, golden[f"ring_{n}_{L}_out"])
+
+
+@pytest.mark.parametrize("n,L,root", [(8, 513, 0), (4, 100, 2), (4, 4099, 3)])
+def test_reduce_bcast_matches_reference(golden, n, L, root):
+    for r in run(n, list(golden[f"rb_{n}_{L}_{root}_in"]), "reduce_bcast", root=root):
+        assert np.array_equal(r, golden[f"rb_{n}_{L}_{root}_out"])
+
+
+def test_exact_small_values():
+    out = run(2, [np.array([1, 2], np.float32), np.array([10, 20], np.float32)], "multicolor",
+              tree_set=build_multicolor_trees(2, 1, 4))
+    assert [o.tolist() for o in out] == [[11.0, 22.0], [11.0, 22.0]]
+    out = run(8, [np.full(10, r, np.float32) for r in range(8)], "multicolor")
+    assert all((o == 28).all() for o in out)
+
+
+def test_segmentation_does_not_change_bits(golden):
+    inp = list(golden["mc_8_10007_4_4_in"])
+    ts = build_multicolor_trees(8, 4, 4)
+    outs = [run(8, inp, "multicolor", tree_set=ts, segment_elems=s)[3] for s in (1, 17, 250, 1 << 20)]
+    for o in outs:
+        assert np.array_equal(o, golden["mc_8_10007_4_4_out"])
+
+
+def test_back_to_back_calls_reuse_flags_safely():
+    ts = build_multicolor_trees(4, 4)
+
+    def prog(ep):
+        a = allreduce_multicolor(ep, GradientBuffer.of([float(ep.rank)], device=ep.torch_device), ts)
+        first = float(a.data[0])
+        b = allreduce_multicolor(ep, GradientBuffer.of([first], device=ep.torch_device), ts)
+        return float(b.data[0])
+
+    assert run_ranks(4, "cuda", prog, emulate=True).results == [24.0] * 4
+
+
+def test_host_numpy_buffers_are_a_drop_in(golden):
+    """Reference callers pass numpy arrays; the result lands back in them."""
+    inp = golden["mc_8_997_4_4_in"]
+    ts = build_multicolor_trees(8, 4, 4)
+
+    def prog(ep):
+        host = inp[ep.rank].copy()
+        buf = GradientBuffer(host)
+        allreduce_multicolor(ep, buf, ts, segment_elems=64)
+        return host
+
+    for r in run_ranks(8, "cuda", prog, emulate=True).results:
+        assert np.array_equal(r, golden["mc_8_997_4_4_out"])
+
+
+def test_mismatched_lengths_raise():
+    def prog(ep):
+        allreduce(ep, GradientBuffer.zeros(4 if ep.rank else 5, device=ep.torch_device), "ring")
+
+    with pytest.raises(errors.LengthMismatch):
+        run_ranks(2, "cuda", prog, emulate=True)
+
+
+def test_one_rank_identity_and_bad_args():
+    res = run_ranks(1, "cuda", lambda ep: allreduce(
+        ep, GradientBuffer.of([3.5, 4.5], device=ep.torch_device), "multicolor").data.tolist()).results
+    assert res == [[3.5, 4.5]]
+
+    def prog(ep):
+        with pytest.raises(errors.InvalidConfig):
+            allreduce(ep, GradientBuffer.zeros(4, device=ep.torch_device), "butterfly")
+        with pytest.raises(errors.InvalidConfig):
+            allreduce_multicolor(ep, GradientBuffer.zeros(4, device=ep.torch_device),
+                                 build_multicolor_trees(8, 4))
+
+    run_ranks(4, "cuda", prog, emulate=True)
+
+
+@pytest.mark.parametrize("n,k,arity", [(4, 4, 4), (8, 4, 4), (8, 8, 7), (2, 1, 4)])
+@pytest.mark.parametrize("mu,wd", [(0.0, 0.0), (0.9, 1e-4)])
+def test_fused_accumulation_allreduce_and_update(oracle, n, k, arity, mu, wd):
+    """Worker fold -> tree fold -> SGD epilogue in ONE launch == the unfused
+    reference pipeline (node_gradient, allreduce, sub_scaled_f32 [+ momentum])."""
+    rng = np.random.default_rng(n * 100 + k + int(mu * 10))
+    P, m = 100_003, 3
+    workers = [[rng.standard_normal(P).astype(np.float32) for _ in range(m)] for _ in range(n)]
+    w0 = rng.standard_normal(P - 2).astype(np.float32)
+    v0 = rng.standard_normal(P - 2).astype(np.float32)
+    c, wd_b = 0.1 / 128, float(np.float32(wd * 128))
+    tables = oracle.tables_from_trees(n, oracle.trees(n, k, arity))
+    folded = []
+    for r in range(n):
+        acc = workers[r][0].copy()
+        for j in range(1, m):
+            acc += workers[r][j]
+        folded.append(acc)
+    g = oracle.fold_c(tables, folded)
+    want_w, want_v = oracle.sgd_np(w0, g[: P - 2], v0.copy() if mu else None, c, mu, wd_b)
+    ts = build_multicolor_trees(n, k, arity)
+
+    def prog(ep):
+        dev = ep.torch_device
+        buf = GradientBuffer.alloc(P, ep)
+        wk = [torch.from_numpy(x).to(dev) for x in workers[ep.rank]]
+        w = torch.from_numpy(w0.copy()).to(dev)
+        v = torch.from_numpy(v0.copy()).to(dev)
+        upd = SgdUpdate(weights=w, c=c, momentum=v, mu=mu, wd_b=wd_b, update_len=P - 2)
+        allreduce(ep, buf, "multicolor", tree_set=ts, workers=wk, update=upd)
+        return buf.data.cpu().numpy(), w.cpu().numpy(), v.cpu().numpy()
+
+    for gb, w, v in run_ranks(n, "cuda", prog, emulate=True).results:
+        assert np.array_equal(gb, g)
+        assert np.array_equal(w, want_w)
+        if mu:
+            assert np.array_equal(v, want_v)
+
+
+@pytest.mark.parametrize("n,k,arity", [(4, 4, 4), (8, 4, 4)])
+def test_full_resnet50_size_bitwise(oracle, n, k, arity):
+    """25.6M floats (BASELINE config C1 at N=4; C3 tree at N=8), bit-exact."""
+    P = 25_600_000
+    rng = np.random.default_rng(99)
+    arrays = [rng.standard_normal(P, dtype=np.float32) for _ in range(n)]
+    want = oracle.fold_c(oracle.tables_from_trees(n, oracle.trees(n, k, arity)), arrays)
+    ts = build_multicolor_trees(n, k, arity)
+
+    def prog(ep):
+        buf = GradientBuffer.alloc(P, ep)
+        buf.data.copy_(torch.from_numpy(arrays[ep.rank]))
+        allreduce(ep, buf, "multicolor", tree_set=ts)
+        return bool(torch.equal(buf.data.cpu(), torch.from_numpy(want)))
+
+    assert all(run_ranks(n, "cuda", prog, emulate=True).results)
+
+
+def test_closed_form_check_of_reference_bench_fill(oracle):
+    """bench.py's deterministic fill has a closed-form f64 sum: rel err <= 1e-5."""
+    import ctypes as C  # noqa: F401
+
+    from paper_1711_00705_b200 import _lib
+
+    P, n = 4_000_000, 8
+
+    def prog(ep):
+        buf = GradientBuffer.alloc(P, ep)
+        _lib.check(_lib.load().md_fill_rank_input(buf.data.data_ptr(), P, ep.rank, n,
+                                                  _lib.stream_ptr(ep.stream)))
+        allreduce(ep, buf, "multicolor")
+        idx = np.arange(0, P, 997 * 13)
+        got = buf.data.cpu().numpy()[idx].astype(np.float64)
+        return float(np.max(np.abs(got - oracle.expected_fill_sum(idx, n)) / oracle.expected_fill_sum(idx, n)))
+
+    assert max(run_ranks(n, "cuda", prog, emulate=True).results) <= 1e-5
+
+
+# -- one GPU per rank (NVLink P2P) --------------------------------------------------------------
+
+
+@pytest.mark.multigpu
+@need_gpus(2)
+@pytest.mark.parametrize("n,L,k,arity", [(2, 4099, 1, 4), (2, 4099, 2, 4), (2, 0, 2, 4)])
+def test_p2p_two_gpus_match_reference(golden, n, L, k, arity):
+    inp = golden[f"mc_{n}_{L}_{k}_{arity}_in"]
+    ts = build_multicolor_trees(n, k, arity)
+    for r in run(n, list(inp), "multicolor", emulate=False, tree_set=ts, segment_elems=64):
+        assert np.array_equal(r, golden[f"mc_{n}_{L}_{k}_{arity}_out"])
+
+
+@pytest.mark.multigpu
+@need_gpus(4)
+@pytest.mark.parametrize("case", ["mc_4_4099_4_4", "mc_4_10007_4_4", "mc_4_4099_1_4", "mc_4_7_4_4"])
+def test_p2p_four_gpus_match_reference(golden, case):
+    inp = golden[case + "_in"]
+    n, _, k, arity = (int(x) for x in case.split("_")[1:])
+    ts = build_multicolor_trees(n, k, arity)
+    for r in run(n, list(inp), "multicolor", emulate=False, tree_set=ts):
+        assert np.array_equal(r, golden[case + "_out"])
+    out = run(4, list(golden["ring_4_4099_in"]), "ring", emulate=False)
+    assert all(np.array_equal(o, golden["ring_4_4099_out"]) for o in out)

@@ -1,0 +1,150 @@
+"""DIMD on the GPU: random_batch and shuffle indices bit-exact with the
+reference (golden), index parity at the full C4 corpus size, and the P2P
+record exchange checked byte for byte on a synthetic corpus."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1711_00705_b200 import dimd, errors, run_ranks
+from paper_1711_00705_b200.dimd import (
+    BatchRequest,
+    parse_index,
+    random_batch,
+    random_batch_device,
+    shard_from_bytes,
+    shuffle_all,
+    shuffle_group,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def ids_of(records):
+    return np.array([int.from_bytes(r.bytes[:4], "little") for r in records], np.int64)
+
+
+def test_random_batch_matches_reference(golden):
+    blob = golden["rb_blob"].tobytes()
+    entries = parse_index(golden["rb_index"].tobytes())
+    store = shard_from_bytes(blob, entries, 0, 1, 1, device=torch.device("cuda", 0))
+    pos = 0
+    for seed, size in zip(golden["rb_seeds"], golden["rb_sizes"]):
+        want = golden["rb_picks"][pos : pos + size]
+        pos += size
+        got = random_batch(store, BatchRequest(int(size), int(seed)))
+        assert np.array_equal(ids_of(got), want)
+        picks = dimd.random_batch_picks(store, BatchRequest(int(size), int(seed)))
+        assert np.array_equal(picks.cpu().numpy(), want)
+
+
+def test_random_batch_edge_cases():
+    dev = torch.device("cuda", 0)
+    one = shard_from_bytes(b"zz", [dimd.IndexEntry(0, 2, 9)], 0, 1, 1, device=dev)
+    assert random_batch(one, BatchRequest(4, 1)) == [dimd.Record(b"zz", 9)] * 4
+    empty = shard_from_bytes(b"", [], 0, 1, 1, device=dev)
+    with pytest.raises(errors.EmptyShard):
+        random_batch(empty, BatchRequest(1, 0))
+
+
+def test_random_batch_large_n_and_fixed_size_gather(oracle):
+    dev = torch.device("cuda", 0)
+    n, L = 160_000, 512
+    st = dimd.synth_store(n, L, 3, 8, 1234, 0, 8, 3, device=dev)
+    for key in (7, 2**63 + 5, oracle.mix64(0, oracle.SAMP_ROLE, 5, 17)):
+        recs, labels, picks = random_batch_device(st, BatchRequest(32, key), L)
+        want = oracle.random_batch_picks(key, n, 32)
+        assert np.array_equal(picks.cpu().numpy(), want)
+        gids = recs[:, :8].contiguous().view(torch.int64).flatten().cpu().numpy()
+        assert np.array_equal(gids, 3 + 8 * want)
+    # uniformity (pkg/tests/test_dimd.py:198-205): 3 sigma on 100000 draws over 10
+    st10 = dimd.synth_store(10, 16, 0, 1, 5, 0, 1, 0, device=dev)
+    p = dimd.random_batch_picks(st10, BatchRequest(100_000, 5)).cpu().numpy()
+    freq = np.bincount(p, minlength=10)
+    assert np.all(np.abs(freq - 10_000) < 3 * (100_000 * 0.09) ** 0.5)
+
+
+@pytest.mark.parametrize("name", ["sh_a", "sh_b", "sh_c", "sh_d", "sh_e", "sh_f", "sh_g"])
+def test_shuffle_matches_reference(golden, name):
+    nrec, nr, gs, m, seed = (int(x) for x in golden[name + "_meta"])
+    blob = golden[name + "_blob"].tobytes()
+    entries = parse_index(golden[name + "_index"].tobytes())
+    fn = shuffle_group if name in ("sh_b", "sh_g") else shuffle_all
+
+    def body(ep):
+        st = shard_from_bytes(blob, entries, ep.rank, ep.n_ranks, gs, device=ep.torch_device)
+        out = fn(ep, st, m_segments=m, seed=seed)
+        recs = out.records()
+        return ids_of(recs), np.array([r.label for r in recs], np.int64)
+
+    res = run_ranks(nr, "cuda", body, emulate=True).results
+    assert np.array_equal(np.array([len(r[0]) for r in res]), golden[name + "_counts"])
+    assert np.array_equal(np.concatenate([r[0] for r in res]), golden[name + "_ids"])
+    assert np.array_equal(np.concatenate([r[1] for r in res]), golden[name + "_labels"])
+
+
+def test_shuffle_all_equals_shuffle_group(golden):
+    blob = golden["sh_b_blob"].tobytes()
+    entries = parse_index(golden["sh_b_index"].tobytes())
+
+    def body(fn):
+        def prog(ep):
+            st = shard_from_bytes(blob, entries, ep.rank, ep.n_ranks, 2, device=ep.torch_device)
+            return ids_of(fn(ep, st, m_segments=2, seed=5).records())
+        return prog
+
+    a = run_ranks(4, "cuda", body(shuffle_all), emulate=True).results
+    g = run_ranks(4, "cuda", body(shuffle_group), emulate=True).results
+    assert all(np.array_equal(x, y) for x, y in zip(a, g))
+
+
+def test_shuffle_rejects_mismatched_group_shape():
+    def prog(ep):
+        st = dimd.synth_store(4, 16, ep.rank, 6, 1, ep.rank // 3, 3, ep.rank % 3,
+                              device=ep.torch_device)
+        with pytest.raises(errors.GroupMismatch):
+            shuffle_all(ep, st, seed=1)
+
+    run_ranks(4, "cuda", prog, emulate=True)
+
+
+@pytest.mark.parametrize("member", [0, 3, 7])
+def test_full_size_index_parity_c4(oracle, member):
+    """C4: 1.28M records over 8 ranks (160,000 each), m = 23 segments --
+    every output slot's source is bit-exact with the reference algorithm."""
+    n_rec = [160_000] * 8
+    seed = oracle.mix64(0, oracle.SHUF_ROLE, 0)
+    fm, fr = dimd.shuffle_plan_device(seed, 0, 8, member, member, 23, n_rec)
+    wm, wr = oracle.shuffle_plan_c(seed, 0, 8, member, member, 23, n_rec)
+    assert np.array_equal(fm.cpu().numpy(), wm)
+    assert np.array_equal(fr.cpu().numpy(), wr)
+
+
+def test_index_parity_non_power_of_two_group(oracle):
+    """S = 3 and 7 exercise Lemire rejection (and its serial fallback)."""
+    for S, n in [(3, 50_001), (7, 30_011), (5, 1)]:
+        n_rec = [n + q for q in range(S)]
+        for member in (0, S - 1):
+            fm, fr = dimd.shuffle_plan_device(99, 2, S, member, 2 * S + member, 4, n_rec)
+            wm, wr = oracle.shuffle_plan_c(99, 2, S, member, 2 * S + member, 4, n_rec)
+            assert np.array_equal(fm.cpu().numpy(), wm) and np.array_equal(fr.cpu().numpy(), wr)
+
+
+def test_exchange_moves_every_byte(oracle):
+    """8 emulated ranks x 20,000 synthetic 4 KiB records: after the P2P
+    shuffle every record is intact, in the reference's order, none lost."""
+    n_local, L, seed, S = 20_000, 4096, 4242, 8
+
+    def prog(ep):
+        st = dimd.synth_store(n_local, L, ep.rank, S, seed, 0, S, ep.rank, device=ep.torch_device)
+        out = shuffle_all(ep, st, m_segments=3, seed=77)
+        bad, gids = dimd.synth_verify(out, seed)
+        return bad, gids.cpu().numpy()
+
+    res = run_ranks(S, "cuda", prog, emulate=True).results
+    assert all(b == 0 for b, _ in res)
+    allg = np.sort(np.concatenate([g for _, g in res]))
+    assert np.array_equal(allg, np.arange(S * n_local))
+    for r, (_, g) in enumerate(res):
+        wm, wr = oracle.shuffle_plan_c(77, 0, S, r, r, 3, [n_local] * S)
+        assert np.array_equal(g, wm + S * wr)
