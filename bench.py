@@ -89,49 +89,54 @@ def tree_config(n: int):
 
 
 class Clocks:
-    """nvidia-smi sampled every 200 ms during the timed region."""
+    """SM clock + throttle reasons of the run's GPUs, polled through NVML (the
+    library nvidia-smi reads) every ~1 ms by a thread during the timed region
+    -- the region is milliseconds long, below nvidia-smi's sampling period."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # NVML clocks-event bits -> the recipe's names
+        "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+        "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80,
+    }
 
     def __init__(self, gpus):
         self.gpus = gpus
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+        self.sm: list[float] = []
+        self.mask = 0
+        self.run = False
+        self.err = None
+        self.max_mhz = None
+
+    def _loop(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            hs = [nv.nvmlDeviceGetHandleByIndex(i) for i in self.gpus]
+            self.max_mhz = max(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM) for h in hs)
+            while self.run:
+                for h in hs:
+                    self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                    self.mask |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                time.sleep(0.001)
+            nv.nvmlShutdown()
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
 
     def start(self):
-        try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except OSError:
-            self.p = None
+        self.run = True
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+        time.sleep(0.05)  # NVML init before the timed region starts
 
     def stop(self) -> dict:
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        rows = [r.split(",") for r in Path(self.f.name).read_text().splitlines() if r.strip()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], [], set()
-        for r in rows:
-            r = [x.strip() for x in r]
-            try:
-                if int(r[0]) not in self.gpus:
-                    continue
-                sm.append(float(r[1]))
-                mx.append(float(r[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, r[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        self.run = False
+        self.t.join(timeout=5)
+        if self.err and not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml: {self.err}"]}
+        reasons = [k for k, bit in self.REASONS.items() if self.mask & bit]
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.sm),
+                "source": "NVML, 1 ms polling during the timed region"}
 
 
 # -- our implementation ------------------------------------------------------------------------------

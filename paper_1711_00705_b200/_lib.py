@@ -113,10 +113,17 @@ def check(rc: int) -> None:
     raise cls(msg or f"libmdb200 error {rc}")
 
 
+def _addr(p) -> int | None:
+    if isinstance(p, C.c_void_p):
+        return p.value
+    return int(p) if p else None
+
+
 def ptr_array(ptrs) -> C.Array:
+    """Host array of device addresses (ints or opaque c_void_p handles)."""
     arr = (C.c_void_p * max(1, len(ptrs)))()
     for i, p in enumerate(ptrs):
-        arr[i] = int(p) if p else None
+        arr[i] = _addr(p)
     return arr
 
 

@@ -476,7 +476,9 @@ __global__ void __launch_bounds__(kArThreads, 1)
       __syncthreads();
       continue;
     }
-    if (t.type == 0 && t.is_leaf && a.n_workers == 0) {  // leaf data ready at entry
+    // a non-root leaf without a worker fold has nothing to do: its data was
+    // ready at the entry barrier (a lone root still runs its epilogue)
+    if (t.type == 0 && t.is_leaf && t.parent >= 0 && a.n_workers == 0) {
       __syncthreads();
       continue;
     }

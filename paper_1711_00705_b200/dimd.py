@@ -405,6 +405,19 @@ def shuffle_group(ep, store: ShardStore, m_segments: int | None = None, seed: in
     return _shuffle(ep, store, m_segments, seed)
 
 
+def group_record_counts(channel, members, n_records: int, m_segments: int) -> list[int]:
+    """Host step of the shuffle (collective over every world rank): gather the
+    members' record counts -- all a receiver needs to recompute every source's
+    destination draws -- and insist the group agrees on m_segments (dest keys
+    depend on the segment index, dimd.py:308; the reference would deadlock
+    on a disagreement, here it is an InvalidConfig on every member)."""
+    rows = channel.all_gather((int(n_records), int(m_segments)))
+    seen = [rows[m][1] for m in members]
+    if any(x != m_segments for x in seen):
+        raise InvalidConfig(f"group members disagree on m_segments: {seen}")
+    return [rows[m][0] for m in members]
+
+
 def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     S = store.group_size
     if S > _lib.MD_MAX_GROUP:
@@ -420,13 +433,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     members = list(range(first, first + S))
     # make every source's shard visible (sync: the blob must be complete)
     torch.cuda.current_stream(dev).synchronize()
-    rows = ep.all_gather((store.n_records, int(m_segments)))
-    for m in members:
-        if rows[m][1] != m_segments:
-            raise InvalidConfig(
-                f"group members disagree on m_segments: {[rows[x][1] for x in members]}"
-            )
-    n_rec = [rows[m][0] for m in members]
+    n_rec = group_record_counts(ep, members, store.n_records, int(m_segments))
     v_blob = ep.register_varlen(store.blob)
     v_off = ep.register_varlen(store.off if store.n_records else torch.zeros(1, dtype=torch.int64, device=dev))
     v_len = ep.register_varlen(store.length if store.n_records else torch.zeros(1, dtype=torch.int32, device=dev))

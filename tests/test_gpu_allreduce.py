@@ -161,6 +161,39 @@ def test_fused_accumulation_allreduce_and_update(oracle, n, k, arity, mu, wd):
             assert np.array_equal(v, want_v)
 
 
+@pytest.mark.parametrize("workers", [0, 2])
+@pytest.mark.parametrize("mu,wd", [(0.0, 0.0), (0.9, 1e-4)])
+def test_single_rank_fused_update(oracle, workers, mu, wd):
+    """N = 1: the collective is the identity but the fused epilogue (and the
+    worker fold) must still run -- the bench's one-GPU configuration."""
+    rng = np.random.default_rng(17)
+    P = 1_000_003
+    g0 = rng.standard_normal(P).astype(np.float32)
+    wk = [rng.standard_normal(P).astype(np.float32) for _ in range(workers)]
+    w0 = rng.standard_normal(P - 2).astype(np.float32)
+    v0 = rng.standard_normal(P - 2).astype(np.float32)
+    c, wd_b = 0.1 / 32, float(np.float32(wd * 32))
+    g = g0 if not workers else (wk[0] + wk[1])
+    want_w, want_v = oracle.sgd_np(w0, g[: P - 2], v0.copy() if mu else None, c, mu, wd_b)
+
+    def prog(ep):
+        dev = ep.torch_device
+        buf = GradientBuffer.alloc(P, ep)
+        buf.data.copy_(torch.from_numpy(g0))
+        w = torch.from_numpy(w0.copy()).to(dev)
+        v = torch.from_numpy(v0.copy()).to(dev)
+        allreduce(ep, buf, "multicolor",
+                  workers=[torch.from_numpy(x).to(dev) for x in wk] or None,
+                  update=SgdUpdate(weights=w, c=c, momentum=v, mu=mu, wd_b=wd_b, update_len=P - 2))
+        return buf.data.cpu().numpy(), w.cpu().numpy(), v.cpu().numpy()
+
+    gb, w, v = run_ranks(1, "cuda", prog).results[0]
+    assert np.array_equal(gb, g)
+    assert np.array_equal(w, want_w)
+    if mu:
+        assert np.array_equal(v, want_v)
+
+
 @pytest.mark.parametrize("n,k,arity", [(4, 4, 4), (8, 4, 4)])
 def test_full_resnet50_size_bitwise(oracle, n, k, arity):
     """25.6M floats (BASELINE config C1 at N=4; C3 tree at N=8), bit-exact."""
