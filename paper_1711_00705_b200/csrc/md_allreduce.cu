@@ -907,6 +907,12 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   int64_t seg = std::max<int64_t>(4, (seg_elems + 3) & ~int64_t(3));
   int64_t min_seg = ((maxlen + 3) / kMaxSegs + 4 + 3) & ~int64_t(3);
   if (seg < min_seg) seg = min_seg;
+  if (N == 1) {
+    // nothing to pipeline against: ~2 items per SM amortise the per-item
+    // queue/flag overhead of the streaming SGD epilogue
+    int64_t big = ((maxlen / (2 * sm_count(0)) + 1023) / 1024) * 1024;
+    seg = std::max(seg, big);
+  }
   a.seg = seg;
   int64_t mx = 0;
   for (int col = 0; col < plan->k; ++col) {
