@@ -42,7 +42,11 @@ from paper_1711_00705_b200.topology import (
 )
 
 PIPELINE_DEPTH = 4             # reference constant (collectives.py:39); unused on device
-DEFAULT_SEGMENT_ELEMS = 16384  # collectives.py:40; the device pipeline granularity
+# Device pipeline granularity (elements per flag). The reference uses 16384
+# (64 KiB host messages, collectives.py:40); bits do not depend on it, and on
+# B200 256 KiB segments amortise the per-item flag/queue cost (measured: see
+# profiles/README.md).
+DEFAULT_SEGMENT_ELEMS = 65536
 ALGORITHMS = ("multicolor", "ring", "reduce_bcast")
 
 _MAX_SLICE = 1 << 31

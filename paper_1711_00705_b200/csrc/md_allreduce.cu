@@ -102,6 +102,7 @@ struct AllreduceArgs {
   unsigned long long timeout_ns;
   int32_t n_ranks, k, n_views, ctas_per_view;
   int32_t max_nseg, n_workers;
+  int32_t lag, max_stage;  // queue skew between pipeline stages (segments)
   int32_t has_update, vec_ok;
   float c, mu, wd_b;
   ViewArgs v[MD_MAX_RANKS];
@@ -283,86 +284,188 @@ __device__ __forceinline__ typename Elem<kVec>::T own_value(const AllreduceArgs&
   return x;
 }
 
-// Process elements [lo, hi) (all W-aligned when kVec) of one item. kEpi is
-// the epilogue variant where this item makes a segment final, 0 elsewhere.
+// ---- TMA path: remote sources stream through a shared-memory ring -------------
+// One elected thread issues cp.async.bulk copies of every remote fold source
+// (children's subtree sums, or the parent's final segment) straight from the
+// peers' HBM over NVLink into a kStages-deep ring; all threads fold the ring
+// contents with the own value in the reference order, store, and run the SGD
+// epilogue while the next chunks are in flight. Bytes in flight per SM are
+// bounded by the ring (3 x 32 KB), not by registers, and the HBM epilogue
+// overlaps the NVLink transfer instead of alternating with it.
+constexpr int kStages = 4;
+constexpr uint32_t kStageBytes = 32 * 1024;
+constexpr uint32_t kRingBytes = kStages * kStageBytes;
+
+template <int kEpi>
+__device__ __forceinline__ void item_tma(const AllreduceArgs& a, const ViewArgs& v, const Task& t,
+                                         bool final_here, int64_t lo, int64_t hi, int nrem,
+                                         char* ring, uint64_t* full, uint32_t& seq) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  // elements per remote source per stage (multiple of 4 -> 16-byte TMA sizes)
+  const int64_t C = static_cast<int64_t>(kStageBytes / (4u * nrem)) & ~int64_t(3);
+  const int64_t nch = (hi - lo + C - 1) / C;
+  auto issue = [&](int64_t c) {  // thread 0 only
+    const uint32_t g = seq + static_cast<uint32_t>(c);
+    uint64_t* bar = &full[g % kStages];
+    char* stage = ring + (g % kStages) * kStageBytes;
+    const int64_t clo = lo + c * C;
+    const uint32_t bytes = static_cast<uint32_t>((min(hi, clo + C) - clo) * 4);
+    mbar_expect_tx(bar, bytes * nrem);
+    if (t.type == 1) {
+      tma_load_1d(stage, v.peer[t.parent] + clo, bytes, bar);
+    } else {
+      int q = 0;
+      for (int j = 0; j < t.n_fold; ++j) {
+        const int src = t.fold_src[j];
+        if (src == v.rank) continue;
+        tma_load_1d(stage + q * C * 4, v.peer[src] + clo, bytes, bar);
+        ++q;
+      }
+    }
+  };
+  if (tid == 0) {
+    fence_proxy_async_global();  // peers' flags were acquired in the generic proxy
+    for (int64_t c = 0; c < nch && c < kStages; ++c) issue(c);
+  }
+  for (int64_t c = 0; c < nch; ++c) {
+    const uint32_t g = seq + static_cast<uint32_t>(c);
+    const char* stage = ring + (g % kStages) * kStageBytes;
+    while (!mbar_try_wait(&full[g % kStages], (g / kStages) & 1)) {
+    }
+    const int64_t clo = lo + c * C;
+    const int64_t chi = min(hi, clo + C);
+    const int64_t n4 = (chi - clo) / 4;
+    for (int64_t e0 = tid; e0 < n4; e0 += static_cast<int64_t>(kUnroll) * nthr) {
+      const int64_t b = clo + 4 * e0;
+      float4 acc[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t e = e0 + static_cast<int64_t>(u) * nthr;
+        if (e >= n4) break;
+        if (t.type == 1) {
+          acc[u] = reinterpret_cast<const float4*>(stage)[e];
+        } else {
+          int q = 0;
+          for (int j = 0; j < t.n_fold; ++j) {
+            float4 x;
+            if (t.fold_src[j] == v.rank) {
+              x = own_value<true>(a, v, clo + 4 * e);
+            } else {
+              x = reinterpret_cast<const float4*>(stage + q * C * 4)[e];
+              ++q;
+            }
+            acc[u] = (j == 0) ? x : add4(acc[u], x);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t e = e0 + static_cast<int64_t>(u) * nthr;
+        if (e < n4) *reinterpret_cast<float4*>(v.buf + clo + 4 * e) = acc[u];
+      }
+      if (kEpi != 0 && final_here) epi_batch<true, kEpi>(a, v, b, chi, nthr, acc);
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (tid == 0 && c + kStages < nch) issue(c + kStages);
+  }
+  seq += static_cast<uint32_t>(nch);
+}
+
+// Epilogue pass over [lo, hi): every thread re-reads the elements it just
+// stored (same mapping, so program order makes them visible; they are still
+// in L2) and updates W (+ momentum). Kept out of the data pass so the fold's
+// in-flight loads do not compete with the epilogue's registers.
 template <bool kVec, int kEpi>
+__device__ __forceinline__ void epilogue_pass(const AllreduceArgs& a, const ViewArgs& v,
+                                              int64_t lo, int64_t hi, int tid, int nthr) {
+  if constexpr (kEpi != 0) {
+    using E = Elem<kVec>;
+    constexpr int W = E::W;
+    const int64_t step = static_cast<int64_t>(nthr) * W * kUnroll;
+    for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
+      typename E::T g[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        int64_t i = b + static_cast<int64_t>(u) * nthr * W;
+        if (i < hi) g[u] = E::ld(v.buf, i);
+      }
+      epi_batch<kVec, kEpi>(a, v, b, hi, nthr, g);
+    }
+  }
+}
+
+// Data pass of one item over [lo, hi) (all W-aligned when kVec): DOWN copies
+// the parent's final segment, UP folds its sources in the plan's order.
+template <bool kVec>
 __device__ __forceinline__ void item_data(const AllreduceArgs& a, const ViewArgs& v, const Task& t,
                                           int64_t lo, int64_t hi, int tid, int nthr) {
   using E = Elem<kVec>;
   constexpr int W = E::W;
-  const int64_t step = static_cast<int64_t>(nthr) * W * kUnroll;
+  constexpr int kCopyUnroll = 2 * kUnroll;  // a copy holds nothing else in registers
   if (t.type == 1) {  // DOWN: copy the parent's final value
     const float* src = v.peer[t.parent];
-    for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
-      typename E::T x[kUnroll];
+    const int64_t cstep = static_cast<int64_t>(nthr) * W * kCopyUnroll;
+    for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += cstep) {
+      typename E::T x[kCopyUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < kCopyUnroll; ++u) {
         int64_t i = b + static_cast<int64_t>(u) * nthr * W;
         if (i < hi) x[u] = E::ld(src, i);
       }
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
+      for (int u = 0; u < kCopyUnroll; ++u) {
         int64_t i = b + static_cast<int64_t>(u) * nthr * W;
         if (i < hi) E::st(v.buf, i, x[u]);
       }
-      epi_batch<kVec, kEpi>(a, v, b, hi, nthr, x);
     }
     return;
   }
-  if (t.n_fold == 1 && a.n_workers == 0) {  // lone rank: the sum is the buffer itself
-    if constexpr (kEpi != 0) {
-      for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
-        typename E::T g[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          int64_t i = b + static_cast<int64_t>(u) * nthr * W;
-          if (i < hi) g[u] = E::ld_stream(v.buf, i);
-        }
-        epi_batch<kVec, kEpi>(a, v, b, hi, nthr, g);
-      }
-    }
-    return;
-  }
+  if (t.n_fold == 1 && a.n_workers == 0) return;  // lone rank: the sum is the buffer
   // UP: fold own value and children in the plan's order
+  const int64_t step = static_cast<int64_t>(nthr) * W * kUnroll;
+  constexpr int kGroup = 4;  // fold sources whose loads are in flight together
   for (int64_t b = lo + static_cast<int64_t>(tid) * W; b < hi; b += step) {
     typename E::T acc[kUnroll];
-    for (int j = 0; j < t.n_fold; ++j) {
-      const int src_rank = t.fold_src[j];
-      typename E::T x[kUnroll];
-      if (src_rank == v.rank) {
+    for (int j0 = 0; j0 < t.n_fold; j0 += kGroup) {
+      typename E::T x[kGroup][kUnroll];
+      // issue every load of the group first (remote latency ~2 us) ...
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        const int j = j0 + q;
+        if (j >= t.n_fold) break;
+        const int src_rank = t.fold_src[j];
+        const float* src = src_rank == v.rank ? nullptr : v.peer[src_rank];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           int64_t i = b + static_cast<int64_t>(u) * nthr * W;
-          if (i < hi) x[u] = own_value<kVec>(a, v, i);
-        }
-      } else {
-        const float* src = v.peer[src_rank];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          int64_t i = b + static_cast<int64_t>(u) * nthr * W;
-          if (i < hi) x[u] = E::ld(src, i);
+          if (i < hi) x[q][u] = src ? E::ld(src, i) : own_value<kVec>(a, v, i);
         }
       }
+      // ... then add strictly in the reference's fold order
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) acc[u] = (j == 0) ? x[u] : E::add(acc[u], x[u]);
+      for (int q = 0; q < kGroup; ++q) {
+        const int j = j0 + q;
+        if (j >= t.n_fold) break;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) acc[u] = (j == 0) ? x[q][u] : E::add(acc[u], x[q][u]);
+      }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       int64_t i = b + static_cast<int64_t>(u) * nthr * W;
       if (i < hi) E::st(v.buf, i, acc[u]);
     }
-    epi_batch<kVec, kEpi>(a, v, b, hi, nthr, acc);
   }
 }
 
 // The kernel is instantiated per epilogue variant (chosen on the host for the
-// whole call); items that do not make a segment final run variant 0.
+// whole call); the epilogue runs where an item makes a segment final.
 template <bool kVec, int kEpi>
 __device__ __forceinline__ void item_dispatch(const AllreduceArgs& a, const ViewArgs& v,
                                               const Task& t, bool final_here, int64_t lo,
                                               int64_t hi, int tid, int nthr) {
-  if (kEpi != 0 && final_here) item_data<kVec, kEpi>(a, v, t, lo, hi, tid, nthr);
-  else item_data<kVec, 0>(a, v, t, lo, hi, tid, nthr);
+  item_data<kVec>(a, v, t, lo, hi, tid, nthr);
+  if (kEpi != 0 && final_here) epilogue_pass<kVec, kEpi>(a, v, lo, hi, tid, nthr);
 }
 
 // Entry barrier + length agreement. Returns false if this view must skip work.
@@ -451,12 +554,25 @@ __global__ void __launch_bounds__(kArThreads, 1)
   // the epoch lives in the control block (device side), so a captured CUDA
   // graph can replay this launch: every call bumps it exactly once
   __shared__ uint32_t s_epoch;
-  if (tid == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
+  __shared__ __align__(8) uint64_t tma_full[kStages];
+  extern __shared__ __align__(128) char ring[];  // kRingBytes of TMA stages
+  uint32_t tma_seq = 0;                          // chunks through the ring so far
+  if (tid == 0) {
+    s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
+    for (int s = 0; s < kStages; ++s) mbar_init(&tma_full[s], 1);
+    mbar_init_fence();
+  }
   __syncthreads();
   const uint32_t epoch = s_epoch;
   bool ok = entry_barrier(a, v, local_cta, epoch);
   const int n_tasks = rp.n_tasks;
-  const int64_t n_items = static_cast<int64_t>(a.max_nseg) * n_tasks;
+  // queue order: "time" tau, then task (tasks are sorted by stage); task t
+  // works on segment tau - lag * stage(t), so a consumer is handed its
+  // segment about `lag` segments after the producer stage was handed it --
+  // late enough that its flag is usually already set. Producers always come
+  // strictly earlier in this order, which keeps flag waits deadlock free.
+  const int64_t n_items =
+      static_cast<int64_t>(a.max_nseg + a.lag * a.max_stage) * n_tasks;
   __shared__ int64_t s_item;
   __shared__ int s_go;
 
@@ -468,11 +584,11 @@ __global__ void __launch_bounds__(kArThreads, 1)
     __syncthreads();
     const int64_t item = s_item;
     if (item >= n_items) break;
-    const int s = static_cast<int>(item / n_tasks);
     const Task& t = rp.t[item % n_tasks];
+    const int s = static_cast<int>(item / n_tasks) - a.lag * t.stage;
     int64_t cstart, clen;
     chunk_of(a.n, a.k, t.color, &cstart, &clen);
-    if (s >= nseg_of(cstart, clen, a.seg)) {
+    if (s < 0 || s >= nseg_of(cstart, clen, a.seg)) {
       __syncthreads();
       continue;
     }
@@ -508,7 +624,11 @@ __global__ void __launch_bounds__(kArThreads, 1)
     const int64_t vlo = min(hi, (lo + 3) & ~int64_t(3));
     const int64_t vhi = max(vlo, hi & ~int64_t(3));
     if (a.vec_ok) {
-      item_dispatch<true, kEpi>(a, v, t, final_here, vlo, vhi, tid, nthr);
+      const int nrem = t.type == 1 ? 1 : t.n_fold - 1;  // UP folds always hold the own value
+      if (nrem >= 1 && vhi > vlo)
+        item_tma<kEpi>(a, v, t, final_here, vlo, vhi, nrem, ring, tma_full, tma_seq);
+      else
+        item_dispatch<true, kEpi>(a, v, t, final_here, vlo, vhi, tid, nthr);
       if (tid < 8) {  // <= 3 head + <= 3 tail scalars
         int64_t i = (tid < 4) ? lo + tid : vhi + (tid - 4);
         bool mine = (tid < 4) ? (i < vlo) : (i < hi);
@@ -971,7 +1091,16 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     case 4: kern = reinterpret_cast<const void*>(allreduce_kernel<4>); break;
     default: kern = reinterpret_cast<const void*>(allreduce_kernel<0>); break;
   }
-  MD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArThreads, 0));
+  // the attribute lives in each device's context: remember it per device
+  static std::atomic<uint32_t> smem_set[64];
+  const uint32_t bit = 1u << epi;
+  if (dev < 0 || dev >= 64 || !(smem_set[dev].load() & bit)) {
+    MD_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kRingBytes)));
+    if (dev >= 0 && dev < 64) smem_set[dev].fetch_or(bit);
+  }
+  MD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArThreads,
+                                                             kRingBytes));
   int resident = per_sm * sm_count(dev);
   if (ctas <= 0) ctas = resident / n_views;
   ctas = std::min(ctas, resident / n_views);
@@ -980,12 +1109,22 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     return MD_ERR_INVALID_CONFIG;
   }
   a.ctas_per_view = ctas;
+  // lag: about one CTA wave of items per pipeline stage (override: MD_AR_LAG)
+  int max_stage = 0, max_tasks = 1;
+  for (const RankPlan& rp : plan->host) {
+    max_tasks = std::max(max_tasks, rp.n_tasks);
+    for (int i = 0; i < rp.n_tasks; ++i) max_stage = std::max(max_stage, rp.t[i].stage);
+  }
+  int lag = std::max(1, ctas / max_tasks);
+  if (const char* e = getenv("MD_AR_LAG")) lag = std::max(0, atoi(e));
+  a.lag = lag;
+  a.max_stage = max_stage;
   void* args[] = {&a};
   // cooperative launch: every CTA (of every emulated rank) co-resident, so
   // flag waits between CTAs can never deadlock on scheduling
   MD_CUDA_TRY(cudaLaunchCooperativeKernel(kern,
-                                          dim3(ctas * n_views), dim3(kArThreads), args, 0,
-                                          as_stream(stream)));
+                                          dim3(ctas * n_views), dim3(kArThreads), args,
+                                          kRingBytes, as_stream(stream)));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return MD_OK;
 }
