@@ -1,0 +1,112 @@
+#!/usr/bin/env python3
+"""BASELINE config C4: the DIMD store on B200 -- per-epoch shuffle (partition
+exchange over NVLink) and minibatch gather, with bit-exact indices.
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench_dimd.py [--records 160000]
+
+Every rank holds a shard of `--records` synthetic 224x224x3 uint8 records
+(24.08 GB at 160,000; C4 puts 1.28M records on 8 GPUs = 160,000 each),
+striped by the reference rule (dimd.py:192). One `shuffle_all` epoch
+(m_segments = default_segments(shard bytes), as the reference computes it) is
+timed with CUDA events (max over ranks), then every record of the new shard is
+verified against the generator and its source index compared with the CPU
+oracle's plan (numpy-Philox semantics) -- bit-exact indices. Then 1000
+minibatch gathers of 32 records are timed. Prints one JSON line.
+Roofline: the exchange must move (S-1)/S of the shard bytes over NVLink
+(pull) and write every byte once into HBM.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+REC = 224 * 224 * 3
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--records", type=int, default=160_000)
+    ap.add_argument("--gathers", type=int, default=1000)
+    ap.add_argument("--seed", type=int, default=2017)
+    ap.add_argument("--no-verify", action="store_true")
+    a = ap.parse_args()
+
+    import torch
+
+    from oracle import oracle as O
+    from paper_1711_00705_b200 import dimd
+    from paper_1711_00705_b200.dimd import BatchRequest, BatchSlots, random_batch_device
+    from paper_1711_00705_b200.transport import init_from_env
+
+    ep = init_from_env()
+    N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
+    S, n = N, a.records
+    seed = O.mix64(a.seed, O.SHUF_ROLE, 0)  # epoch 0 key, sgd.py:503-506
+    with torch.cuda.stream(ep.stream):
+        store = dimd.synth_store(n, REC, rank, S, a.seed, 0, S, rank, device=dev)
+        torch.cuda.synchronize(dev)
+        m_seg = dimd.default_segments(store.nbytes)
+        ep.barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ep.stream)
+        out = dimd.shuffle_all(ep, store, m_segments=m_seg, seed=seed)
+        e1.record(ep.stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        ev_ms = e0.elapsed_time(e1)
+        n_out = out.n_records
+        del store
+        torch.cuda.empty_cache()
+        bad, exact = -1, None
+        if not a.no_verify:
+            bad, gids = dimd.synth_verify(out, a.seed)
+            mem, rec = O.shuffle_plan_c(seed, 0, S, rank, rank, m_seg, [n] * S)
+            exact = bool(np.array_equal(gids.cpu().numpy(), mem + S * rec))
+        # minibatch gather rate from the new shard
+        slots = BatchSlots(32, REC, dev)
+        for i in range(20):
+            random_batch_device(out, BatchRequest(32, i), REC, slots)
+        torch.cuda.synchronize(dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(ep.stream)
+        for i in range(a.gathers):
+            random_batch_device(out, BatchRequest(32, 1000 + i), REC, slots)
+        g1.record(ep.stream)
+        torch.cuda.synchronize(dev)
+        slots.check()
+        gather_ms = g0.elapsed_time(g1) / a.gathers
+    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms))
+    if rank == 0:
+        wall = max(r[0] for r in rows)
+        total = sum(r[2] for r in rows)
+        nvlink_bytes = n * REC * (S - 1) / S  # expected pulled bytes per GPU
+        line = {
+            "metric": "DIMD shuffle records/s (whole job) and minibatch gather records/s per GPU",
+            "n_gpus": N, "records_per_gpu": n, "record_bytes": REC, "m_segments": m_seg,
+            "shuffle_s": wall, "shuffle_records_per_s": total / wall,
+            "shuffle_GBps_per_gpu": n * REC / wall / 1e9,
+            "nvlink_GBps_per_gpu": nvlink_bytes / wall / 1e9 if S > 1 else None,
+            "hbm_GBps_per_gpu": 2 * n * REC / wall / 1e9,
+            "shuffle_event_ms_max": max(r[1] for r in rows),
+            "records_out": [r[2] for r in rows],
+            "corrupt_records": sum(max(0, r[3]) for r in rows),
+            "indices_bit_exact_vs_oracle": all(r[4] for r in rows) if not a.no_verify else None,
+            "gather_ms_per_batch32": max(r[5] for r in rows),
+            "gather_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
+            "gather_hbm_GBps": 2 * 32 * REC / (max(r[5] for r in rows) / 1e3) / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    ep.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -655,6 +655,273 @@ __global__ void __launch_bounds__(kArThreads, 1)
   exit_barrier(a, v, epoch);
 }
 
+// ---- channelized kernel (vector-aligned buffers) -------------------------------
+// Every CTA owns one task of its rank (UP fold or DOWN copy of one color) and
+// the segments idx, idx + m, idx + 2m, ... of that task's chunk, where the m
+// CTAs of a task are allotted in proportion to its remote bytes. Inside a CTA
+// warp 0 is the producer: it waits for each segment's flags, handles the <= 3
+// unaligned edge elements itself and streams the remote sources through the
+// TMA ring; warps 1.. are consumers: fold (reference order), store, SGD
+// epilogue, and publish the segment's flag. The ring runs continuously across
+// the CTA's segments, so NVLink transfers, HBM epilogue and flag latency all
+// overlap; segments can stay small (fine-grained pipelining across GPUs).
+constexpr int kConsumerWarps = kArThreads / 32 - 1;
+
+__device__ __forceinline__ int task_weight(const AllreduceArgs& a, const Task& t) {
+  if (t.type == 1) return 1;                                   // DOWN: one remote source
+  if (t.n_fold > 1) return t.n_fold - 1;                       // UP with children
+  return (t.parent < 0 || a.n_workers > 0) ? 1 : 0;            // lone root / leaf fold
+}
+
+// Deterministic CTA -> (task, index, count) allotment, identical in every CTA.
+__device__ void allot(const AllreduceArgs& a, const RankPlan& rp, int cta, int* task, int* idx,
+                      int* count) {
+  int m[2 * MD_MAX_COLORS];
+  int w[2 * MD_MAX_COLORS];
+  int W = 0, used = 0;
+  for (int i = 0; i < rp.n_tasks; ++i) {
+    w[i] = task_weight(a, rp.t[i]);
+    W += w[i];
+  }
+  *task = -1;
+  if (W == 0) return;
+  for (int i = 0; i < rp.n_tasks; ++i) {
+    m[i] = w[i] ? max(1, a.ctas_per_view * w[i] / W) : 0;
+    used += m[i];
+  }
+  while (used > a.ctas_per_view) {  // too many tasks for the CTAs: trim the largest
+    int big = 0;
+    for (int i = 1; i < rp.n_tasks; ++i)
+      if (m[i] > m[big]) big = i;
+    if (m[big] <= 1) break;
+    --m[big];
+    --used;
+  }
+  for (int i = 0; used < a.ctas_per_view; i = (i + 1) % rp.n_tasks)  // spread the rest
+    if (w[i]) {
+      ++m[i];
+      ++used;
+    }
+  int base = 0;
+  for (int i = 0; i < rp.n_tasks; ++i) {
+    if (cta < base + m[i]) {
+      *task = i;
+      *idx = cta - base;
+      *count = m[i];
+      return;
+    }
+    base += m[i];
+  }
+}
+
+struct SegGeom {
+  int64_t lo, hi, vlo, vhi, C, nch;
+};
+
+__device__ __forceinline__ SegGeom seg_geom(const AllreduceArgs& a, const Task& t, int s,
+                                            int nrem) {
+  int64_t cstart, clen;
+  chunk_of(a.n, a.k, t.color, &cstart, &clen);
+  const int64_t A = cstart & ~int64_t(3);
+  SegGeom g;
+  g.lo = max(cstart, A + static_cast<int64_t>(s) * a.seg);
+  g.hi = min(cstart + clen, A + static_cast<int64_t>(s + 1) * a.seg);
+  g.vlo = min(g.hi, (g.lo + 3) & ~int64_t(3));
+  g.vhi = max(g.vlo, g.hi & ~int64_t(3));
+  g.C = nrem ? static_cast<int64_t>(kStageBytes / (4u * nrem)) & ~int64_t(3) : 0;
+  g.nch = nrem ? (g.vhi - g.vlo + g.C - 1) / g.C : 0;
+  return g;
+}
+
+// Wait (thread-level) for the producers of segment s of task t.
+__device__ bool wait_inputs(const AllreduceArgs& a, const ViewArgs& v, const Task& t, int s,
+                            uint32_t epoch) {
+  if (t.type == 1) return wait_flag(v, &v.ctrl->down[t.color][s], epoch, a.timeout_ns, 3000 + t.color);
+  for (int j = 0; j < t.n_fold; ++j) {
+    if (t.fold_src[j] == v.rank) continue;
+    if (t.fold_leaf[j] && a.n_workers == 0) continue;
+    if (!wait_flag(v, &v.ctrl->up[t.color][j][s], epoch, a.timeout_ns, 4000 + t.color))
+      return false;
+  }
+  return true;
+}
+
+// Release segment s: up flag in the parent, or down flags in the children.
+__device__ __forceinline__ void publish(const ViewArgs& v, const Task& t, int s, uint32_t epoch) {
+  // st.release.sys is cumulative: it orders every store that precedes it in
+  // causality order -- the other consumer threads' stores via bar.sync, the
+  // producer's edge stores via the mbarrier -- before the flag.
+  if (t.type == 0 && t.parent >= 0) {
+    st_release_sys(&v.peer_ctrl[t.parent]->up[t.color][t.my_slot][s], epoch);
+  } else {
+    for (int c = 0; c < t.n_down; ++c)
+      st_release_sys(&v.peer_ctrl[t.down[c]]->down[t.color][s], epoch);
+  }
+}
+
+__device__ __forceinline__ bool aborted(const ViewArgs& v) {
+  return *reinterpret_cast<volatile uint32_t*>(&v.ctrl->abort_flag) != 0;
+}
+
+template <int kEpi>
+__device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Task& t, int idx,
+                            int m, uint32_t epoch, char* ring, uint64_t* full, uint64_t* empty) {
+  const int tid = threadIdx.x;
+  const bool final_here = (t.type == 1) || (t.parent < 0);
+  const int nrem = t.type == 1 ? 1 : t.n_fold - 1;
+  int64_t cstart, clen;
+  chunk_of(a.n, a.k, t.color, &cstart, &clen);
+  const int nseg = static_cast<int>(nseg_of(cstart, clen, a.seg));
+
+  if (nrem == 0) {  // local-only task (lone root epilogue / leaf worker fold)
+    for (int s = idx; s < nseg; s += m) {
+      SegGeom g = seg_geom(a, t, s, 0);
+      item_dispatch<true, kEpi>(a, v, t, final_here, g.vlo, g.vhi, tid, blockDim.x);
+      if (tid < 8) {
+        int64_t i = (tid < 4) ? g.lo + tid : g.vhi + (tid - 4);
+        bool mine = (tid < 4) ? (i < g.vlo) : (i < g.hi);
+        if (mine) item_dispatch<false, kEpi>(a, v, t, final_here, i, i + 1, 0, 1);
+      }
+      __syncthreads();
+      if (tid == 0 && !(t.type == 0 && t.parent < 0 && t.n_down == 0)) publish(v, t, s, epoch);
+    }
+    return;
+  }
+
+  if (tid < 32) {  // ---------------- producer warp (lane 0 works) ----------------
+    if (tid != 0) return;
+    uint32_t gseq = 0;
+    for (int s = idx; s < nseg; s += m) {
+      SegGeom g = seg_geom(a, t, s, nrem);
+      if (!wait_inputs(a, v, t, s, epoch)) return;
+      fence_proxy_async_global();
+      // unaligned edges (only the first/last segment of a color has any)
+      for (int64_t i = g.lo; i < g.hi; ++i) {
+        if (i >= g.vlo && i < g.vhi) {
+          i = g.vhi - 1;
+          continue;
+        }
+        item_dispatch<false, kEpi>(a, v, t, final_here, i, i + 1, 0, 1);
+      }
+      if (g.nch == 0) {  // nothing for the consumers: release the segment here
+        publish(v, t, s, epoch);
+        continue;
+      }
+      for (int64_t c = 0; c < g.nch; ++c, ++gseq) {
+        const uint32_t st = gseq % kStages;
+        if (gseq >= kStages) {
+          uint32_t spins = 0;
+          while (!mbar_try_wait(&empty[st], ((gseq / kStages) - 1) & 1)) {
+            if ((++spins & 1023) == 0 && aborted(v)) return;
+          }
+        }
+        const int64_t clo = g.vlo + c * g.C;
+        const uint32_t bytes = static_cast<uint32_t>((min(g.vhi, clo + g.C) - clo) * 4);
+        char* stage = ring + st * kStageBytes;
+        mbar_expect_tx(&full[st], bytes * nrem);
+        if (t.type == 1) {
+          tma_load_1d(stage, v.peer[t.parent] + clo, bytes, &full[st]);
+        } else {
+          int q = 0;
+          for (int j = 0; j < t.n_fold; ++j) {
+            const int src = t.fold_src[j];
+            if (src == v.rank) continue;
+            tma_load_1d(stage + q * g.C * 4, v.peer[src] + clo, bytes, &full[st]);
+            ++q;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int ct = tid - 32, nct = kConsumerWarps * 32;
+  uint32_t gseq = 0;
+  for (int s = idx; s < nseg; s += m) {
+    SegGeom g = seg_geom(a, t, s, nrem);
+    if (g.nch == 0) continue;
+    for (int64_t c = 0; c < g.nch; ++c, ++gseq) {
+      const uint32_t st = gseq % kStages;
+      uint32_t spins = 0;
+      while (!mbar_try_wait(&full[st], (gseq / kStages) & 1)) {
+        if ((++spins & 1023) == 0 && aborted(v)) return;
+      }
+      const char* stage = ring + st * kStageBytes;
+      const int64_t clo = g.vlo + c * g.C;
+      const int64_t chi = min(g.vhi, clo + g.C);
+      const int64_t n4 = (chi - clo) / 4;
+      for (int64_t e0 = ct; e0 < n4; e0 += static_cast<int64_t>(kUnroll) * nct) {
+        float4 acc[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t e = e0 + static_cast<int64_t>(u) * nct;
+          if (e >= n4) break;
+          if (t.type == 1) {
+            acc[u] = reinterpret_cast<const float4*>(stage)[e];
+          } else {
+            int q = 0;
+            for (int j = 0; j < t.n_fold; ++j) {
+              float4 x;
+              if (t.fold_src[j] == v.rank) {
+                x = own_value<true>(a, v, clo + 4 * e);
+              } else {
+                x = reinterpret_cast<const float4*>(stage + q * g.C * 4)[e];
+                ++q;
+              }
+              acc[u] = (j == 0) ? x : add4(acc[u], x);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const int64_t e = e0 + static_cast<int64_t>(u) * nct;
+          if (e < n4) *reinterpret_cast<float4*>(v.buf + clo + 4 * e) = acc[u];
+        }
+        if (kEpi != 0 && final_here) epi_batch<true, kEpi>(a, v, clo + 4 * e0, chi, nct, acc);
+      }
+      __syncwarp();
+      if ((ct & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
+    }
+    // all consumer warps are done with segment s: release it
+    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
+    if (ct == 0) publish(v, t, s, epoch);
+  }
+}
+
+template <int kEpi>
+__global__ void __launch_bounds__(kArThreads, 1)
+    allreduce_channels_kernel(const __grid_constant__ AllreduceArgs a) {
+  const int view = blockIdx.x / a.ctas_per_view;
+  const int local_cta = blockIdx.x % a.ctas_per_view;
+  const ViewArgs& v = a.v[view];
+  const RankPlan& rp = a.plan[v.rank];
+  const int tid = threadIdx.x;
+  __shared__ uint32_t s_epoch;
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+  __shared__ int s_task, s_idx, s_m;
+  extern __shared__ __align__(128) char ring[];
+  if (tid == 0) {
+    s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    mbar_init_fence();
+    int task, idx = 0, m = 1;
+    allot(a, rp, local_cta, &task, &idx, &m);
+    s_task = task;
+    s_idx = idx;
+    s_m = m;
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  if (entry_barrier(a, v, local_cta, epoch) && s_task >= 0)
+    run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty);
+  exit_barrier(a, v, epoch);
+}
+
 // ---- plan construction (host) ------------------------------------------------
 static int build_rank_plans(int n, int k, const int32_t* parent, const int32_t* child_ptr,
                             const int32_t* child_idx, const int32_t* self_pos,
@@ -1084,16 +1351,30 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   int epi = 0;
   if (has_update) epi = (a.v[0].mom ? 3 : 1) + (wd_b != 0.f ? 1 : 0);
   const void* kern = nullptr;
+  // 16-byte aligned buffers take the channelized TMA kernel; anything else
+  // the work-queue kernel with its scalar path (MD_AR_QUEUE=1 forces it)
+  // (and only when every task of every rank can own at least one CTA)
+  int weighted = 0;
+  for (const RankPlan& rp : plan->host) {
+    int wt = 0;
+    for (int i = 0; i < rp.n_tasks; ++i) {
+      const Task& t = rp.t[i];
+      wt += t.type == 1 || t.n_fold > 1 || t.parent < 0 || n_workers > 0;
+    }
+    weighted = std::max(weighted, wt);
+  }
+  const int est_ctas = sm_count(dev) / n_views;
+  const bool chan = a.vec_ok && !getenv("MD_AR_QUEUE") && weighted <= est_ctas;
   switch (epi) {
-    case 1: kern = reinterpret_cast<const void*>(allreduce_kernel<1>); break;
-    case 2: kern = reinterpret_cast<const void*>(allreduce_kernel<2>); break;
-    case 3: kern = reinterpret_cast<const void*>(allreduce_kernel<3>); break;
-    case 4: kern = reinterpret_cast<const void*>(allreduce_kernel<4>); break;
-    default: kern = reinterpret_cast<const void*>(allreduce_kernel<0>); break;
+    case 1: kern = chan ? (const void*)allreduce_channels_kernel<1> : (const void*)allreduce_kernel<1>; break;
+    case 2: kern = chan ? (const void*)allreduce_channels_kernel<2> : (const void*)allreduce_kernel<2>; break;
+    case 3: kern = chan ? (const void*)allreduce_channels_kernel<3> : (const void*)allreduce_kernel<3>; break;
+    case 4: kern = chan ? (const void*)allreduce_channels_kernel<4> : (const void*)allreduce_kernel<4>; break;
+    default: kern = chan ? (const void*)allreduce_channels_kernel<0> : (const void*)allreduce_kernel<0>; break;
   }
   // the attribute lives in each device's context: remember it per device
   static std::atomic<uint32_t> smem_set[64];
-  const uint32_t bit = 1u << epi;
+  const uint32_t bit = 1u << (epi + (chan ? 8 : 0));
   if (dev < 0 || dev >= 64 || !(smem_set[dev].load() & bit)) {
     MD_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kRingBytes)));

@@ -56,7 +56,7 @@ def main() -> None:
                 else:
                     os.environ["MD_AR_LAG"] = lag
                 mode = f"{mode}/lag{lag}"
-                for seg in (16384, 65536, 262144):
+                for seg in [int(x) for x in os.environ.get("DIAG_SEGS", "16384,65536,262144").split(",")]:
                     times = []
                     for i in range(12):
                         fill()
