@@ -84,7 +84,8 @@ def main() -> None:
         torch.cuda.synchronize(dev)
         slots.check()
         gather_ms = g0.elapsed_time(g1) / a.gathers
-    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms))
+    phases = dict(dimd.LAST_SHUFFLE_PHASES)
+    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases))
     if rank == 0:
         wall = max(r[0] for r in rows)
         total = sum(r[2] for r in rows)
@@ -104,6 +105,8 @@ def main() -> None:
             "gather_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
             "gather_hbm_GBps": 2 * 32 * REC / (max(r[5] for r in rows) / 1e3) / 1e9,
         }
+        if rows[0][6]:
+            line["phases_s_per_rank"] = [r[6] for r in rows]
         print(json.dumps(line), flush=True)
     ep.barrier()
 

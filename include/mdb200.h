@@ -140,6 +140,12 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
                  float* const* w, float* const* mom, int64_t update_len, float c, float mu,
                  float wd_b, int64_t seg_elems, int32_t ctas, void* stream);
 
+/* Diagnostics: with MD_AR_TRACE=1 in the environment every md_allreduce
+ * records %globaltimer events per CTA (flag waits, chunk arrival, segment
+ * completion, publish); this writes the last call's log on `device` to
+ * `path` (records of {u64 t_ns, u32 cta, u16 event, u16 segment}). */
+int md_trace_dump(int32_t device, const char* path);
+
 /* ---- DIMD store: dimd.py ------------------------------------------------- */
 /* _mix64, dimd.py:226-234 (host, pure). */
 uint64_t md_mix64(const uint64_t* parts, int32_t n);

@@ -60,6 +60,7 @@ SIGNATURES = {
         C.c_int,
         [_pp, _i32, _vp, _pp, _i64, _pp, _i32, _pp, _pp, _i64, _f32, _f32, _f32, _i64, _i32, _vp],
     ),
+    "md_trace_dump": (C.c_int, [_i32, C.c_char_p]),
     "md_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "md_random_batch": (C.c_int, [_u64, _i64, _i64, _vp, _vp]),
     "md_gather": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),

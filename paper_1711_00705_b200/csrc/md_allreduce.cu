@@ -94,6 +94,12 @@ struct ViewArgs {
   uint32_t epoch;
 };
 
+struct TraceEv {
+  unsigned long long t;
+  uint32_t cta;
+  uint16_t ev, seg;
+};
+
 struct AllreduceArgs {
   const RankPlan* plan;
   int64_t n;
@@ -105,6 +111,7 @@ struct AllreduceArgs {
   int32_t lag, max_stage;  // queue skew between pipeline stages (segments)
   int32_t has_update, vec_ok;
   float c, mu, wd_b;
+  struct TraceEv* trace;  // nullable: per-CTA event log (MD_AR_TRACE=1)
   ViewArgs v[MD_MAX_RANKS];
 };
 
@@ -759,6 +766,20 @@ __device__ __forceinline__ void publish(const ViewArgs& v, const Task& t, int s,
   }
 }
 
+// ---- optional tracing: %globaltimer events, producer and consumer halves ----
+constexpr int kTraceHalf = 512;  // events per CTA per role
+enum : uint16_t { EV_WAIT0 = 1, EV_WAIT1, EV_ISSUED, EV_FIRST, EV_DONE, EV_PUB, EV_ENTRY, EV_EXIT };
+
+__device__ __forceinline__ void trace_ev(const AllreduceArgs& a, int role, int& n, uint16_t ev,
+                                         int seg) {
+  if (!a.trace || n >= kTraceHalf) return;
+  TraceEv* e = a.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * kTraceHalf + n++;
+  e->t = globaltimer_ns();
+  e->cta = blockIdx.x;
+  e->ev = ev;
+  e->seg = static_cast<uint16_t>(seg);
+}
+
 __device__ __forceinline__ bool aborted(const ViewArgs& v) {
   return *reinterpret_cast<volatile uint32_t*>(&v.ctrl->abort_flag) != 0;
 }
@@ -791,9 +812,12 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
   if (tid < 32) {  // ---------------- producer warp (lane 0 works) ----------------
     if (tid != 0) return;
     uint32_t gseq = 0;
+    int pn = 0;  // trace events
     for (int s = idx; s < nseg; s += m) {
       SegGeom g = seg_geom(a, t, s, nrem);
+      trace_ev(a, 0, pn, EV_WAIT0, s);
       if (!wait_inputs(a, v, t, s, epoch)) return;
+      trace_ev(a, 0, pn, EV_WAIT1, s);
       fence_proxy_async_global();
       // unaligned edges (only the first/last segment of a color has any)
       for (int64_t i = g.lo; i < g.hi; ++i) {
@@ -831,6 +855,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
           }
         }
       }
+      trace_ev(a, 0, pn, EV_ISSUED, s);
     }
     return;
   }
@@ -838,6 +863,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
   // ---------------- consumer warps ----------------
   const int ct = tid - 32, nct = kConsumerWarps * 32;
   uint32_t gseq = 0;
+  int cn = 0;  // trace events (ct == 0 only)
   for (int s = idx; s < nseg; s += m) {
     SegGeom g = seg_geom(a, t, s, nrem);
     if (g.nch == 0) continue;
@@ -847,6 +873,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
       while (!mbar_try_wait(&full[st], (gseq / kStages) & 1)) {
         if ((++spins & 1023) == 0 && aborted(v)) return;
       }
+      if (c == 0 && ct == 0) trace_ev(a, 1, cn, EV_FIRST, s);
       const char* stage = ring + st * kStageBytes;
       const int64_t clo = g.vlo + c * g.C;
       const int64_t chi = min(g.vhi, clo + g.C);
@@ -885,7 +912,11 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
     }
     // all consumer warps are done with segment s: release it
     asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
-    if (ct == 0) publish(v, t, s, epoch);
+    if (ct == 0) {
+      trace_ev(a, 1, cn, EV_DONE, s);
+      publish(v, t, s, epoch);
+      trace_ev(a, 1, cn, EV_PUB, s);
+    }
   }
 }
 
@@ -917,10 +948,21 @@ __global__ void __launch_bounds__(kArThreads, 1)
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
-  if (entry_barrier(a, v, local_cta, epoch) && s_task >= 0)
+  const bool ok = entry_barrier(a, v, local_cta, epoch);
+  int tn = kTraceHalf - 2;  // kernel-level events in the producer half's last slots
+  if (tid == 0) trace_ev(a, 0, tn, EV_ENTRY, s_task < 0 ? 0xffff : s_task);
+  if (ok && s_task >= 0)
     run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty);
+  __syncthreads();
+  if (tid == 0) trace_ev(a, 0, tn, EV_EXIT, s_task < 0 ? 0xffff : s_task);
   exit_barrier(a, v, epoch);
 }
+
+struct TraceBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0, used = 0;
+};
+static TraceBuf g_trace[64];
 
 // ---- plan construction (host) ------------------------------------------------
 static int build_rank_plans(int n, int k, const int32_t* parent, const int32_t* child_ptr,
@@ -1400,6 +1442,18 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   if (const char* e = getenv("MD_AR_LAG")) lag = std::max(0, atoi(e));
   a.lag = lag;
   a.max_stage = max_stage;
+  a.trace = nullptr;
+  if (getenv("MD_AR_TRACE")) {  // diagnostics: one event log per device, per call
+    const size_t bytes = sizeof(TraceEv) * 2 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
+    if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
+      if (g_trace[dev].ptr) cudaFree(g_trace[dev].ptr);
+      MD_CUDA_TRY(cudaMalloc(&g_trace[dev].ptr, bytes));
+      g_trace[dev].bytes = bytes;
+    }
+    MD_CUDA_TRY(cudaMemsetAsync(g_trace[dev].ptr, 0, bytes, as_stream(stream)));
+    g_trace[dev].used = bytes;
+    a.trace = static_cast<TraceEv*>(g_trace[dev].ptr);
+  }
   void* args[] = {&a};
   // cooperative launch: every CTA (of every emulated rank) co-resident, so
   // flag waits between CTAs can never deadlock on scheduling
@@ -1411,3 +1465,28 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
 }
 
 }  // extern "C"
+
+extern "C" int md_trace_dump(int32_t device, const char* path) {
+  if (device < 0 || device >= 64 || !g_trace[device].ptr) {
+    set_error("no allreduce trace on device %d (set MD_AR_TRACE=1)", device);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  std::vector<char> host(g_trace[device].used);
+  int prev;
+  MD_CUDA_TRY(cudaGetDevice(&prev));
+  MD_CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaMemcpy(host.data(), g_trace[device].ptr, host.size(), cudaMemcpyDeviceToHost);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    set_error("trace copy: %s", cudaGetErrorString(e));
+    return MD_ERR_CUDA;
+  }
+  FILE* f = fopen(path, "wb");
+  if (!f) {
+    set_error("cannot write %s", path);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  fwrite(host.data(), 1, host.size(), f);
+  fclose(f);
+  return MD_OK;
+}

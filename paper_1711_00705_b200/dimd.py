@@ -418,6 +418,32 @@ def group_record_counts(channel, members, n_records: int, m_segments: int) -> li
     return [rows[m][0] for m in members]
 
 
+LAST_SHUFFLE_PHASES: dict[str, float] = {}
+
+
+class _PhaseClock:
+    """Host wall time per shuffle phase (MD_DIMD_TIMING=1: synchronizes
+    between phases and records into LAST_SHUFFLE_PHASES)."""
+
+    def __init__(self, dev):
+        import os
+        import time
+
+        self.on = os.environ.get("MD_DIMD_TIMING") == "1"
+        self.dev, self.time = dev, time
+        self.t = time.perf_counter()
+        if self.on:
+            LAST_SHUFFLE_PHASES.clear()
+
+    def __call__(self, name: str) -> None:
+        if not self.on:
+            return
+        torch.cuda.synchronize(self.dev)
+        now = self.time.perf_counter()
+        LAST_SHUFFLE_PHASES[name] = now - self.t
+        self.t = now
+
+
 def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     S = store.group_size
     if S > _lib.MD_MAX_GROUP:
@@ -433,11 +459,13 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     members = list(range(first, first + S))
     # make every source's shard visible (sync: the blob must be complete)
     torch.cuda.current_stream(dev).synchronize()
+    mark = _PhaseClock(dev)
     n_rec = group_record_counts(ep, members, store.n_records, int(m_segments))
     v_blob = ep.register_varlen(store.blob)
     v_off = ep.register_varlen(store.off if store.n_records else torch.zeros(1, dtype=torch.int64, device=dev))
     v_len = ep.register_varlen(store.length if store.n_records else torch.zeros(1, dtype=torch.int32, device=dev))
     v_lab = ep.register_varlen(store.label if store.n_records else torch.zeros(1, dtype=torch.int32, device=dev))
+    mark("register")
     cap = max(1, sum(n_rec))
     fm = torch.empty(cap, dtype=torch.int32, device=dev)
     fr = torch.empty(cap, dtype=torch.int64, device=dev)
@@ -451,6 +479,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
             n_rec_arr, fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), s,
         )
     )
+    mark("plan")
     n_final = int(nf.value)
     off = torch.empty(max(1, n_final), dtype=torch.int64, device=dev)
     ln = torch.empty(max(1, n_final), dtype=torch.int32, device=dev)
@@ -463,6 +492,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
             n_final, off.data_ptr(), ln.data_ptr(), lb.data_ptr(), C.byref(total), s,
         )
     )
+    mark("index")
     blob = torch.empty(max(1, int(total.value)), dtype=torch.uint8, device=dev)
     _lib.check(
         lib.md_shuffle_pull(
@@ -472,7 +502,9 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
         )
     )
     torch.cuda.current_stream(dev).synchronize()
+    mark("pull")
     ep.barrier()  # every pull from our old shard is done before anyone frees it
+    mark("barrier")
     out = ShardStore(blob, off[:n_final], ln[:n_final], lb[:n_final], store.group_id, S,
                      store.rank_in_group)
     out._nbytes = int(total.value)
