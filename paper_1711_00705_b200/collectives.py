@@ -42,11 +42,11 @@ from paper_1711_00705_b200.topology import (
 )
 
 PIPELINE_DEPTH = 4             # reference constant (collectives.py:39); unused on device
-# Device pipeline granularity (elements per flag). The reference uses 16384
-# (64 KiB host messages, collectives.py:40); bits do not depend on it, and on
-# B200 128 KiB segments balance per-segment flag cost against pipeline depth
-# across GPUs (measured sweep: see profiles/README.md).
-DEFAULT_SEGMENT_ELEMS = 32768
+# Pipeline granularity (elements per flag), the reference's own default
+# (collectives.py:40). Bits do not depend on it; on B200 it is also the
+# measured optimum of the channelized kernel (64 KiB per source per segment;
+# sweep in profiles/README.md).
+DEFAULT_SEGMENT_ELEMS = 16384
 ALGORITHMS = ("multicolor", "ring", "reduce_bcast")
 
 _MAX_SLICE = 1 << 31

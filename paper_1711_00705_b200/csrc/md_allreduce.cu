@@ -112,6 +112,7 @@ struct AllreduceArgs {
   int32_t has_update, vec_ok;
   float c, mu, wd_b;
   struct TraceEv* trace;  // nullable: per-CTA event log (MD_AR_TRACE=1)
+  int32_t flag_gpu_fence;  // publish with fence.acq_rel.gpu + relaxed sys stores
   ViewArgs v[MD_MAX_RANKS];
 };
 
@@ -672,7 +673,11 @@ __global__ void __launch_bounds__(kArThreads, 1)
 // epilogue, and publish the segment's flag. The ring runs continuously across
 // the CTA's segments, so NVLink transfers, HBM epilogue and flag latency all
 // overlap; segments can stay small (fine-grained pipelining across GPUs).
-constexpr int kConsumerWarps = kArThreads / 32 - 1;
+// warp 0: TMA producer, warp 1: notifier (publishes finished segments, so the
+// flag fences never stall the consumers), warps 2..15: consumers
+constexpr int kConsumerWarps = kArThreads / 32 - 2;
+constexpr int kConsumerBase = 64;
+constexpr int kDoneSlots = 8;  // segments a notifier may lag behind the consumers
 
 __device__ __forceinline__ int task_weight(const AllreduceArgs& a, const Task& t) {
   if (t.type == 1) return 1;                                   // DOWN: one remote source
@@ -754,16 +759,41 @@ __device__ bool wait_inputs(const AllreduceArgs& a, const ViewArgs& v, const Tas
 }
 
 // Release segment s: up flag in the parent, or down flags in the children.
-__device__ __forceinline__ void publish(const ViewArgs& v, const Task& t, int s, uint32_t epoch) {
-  // st.release.sys is cumulative: it orders every store that precedes it in
-  // causality order -- the other consumer threads' stores via bar.sync, the
-  // producer's edge stores via the mbarrier -- before the flag.
-  if (t.type == 0 && t.parent >= 0) {
-    st_release_sys(&v.peer_ctrl[t.parent]->up[t.color][t.my_slot][s], epoch);
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Flag stores of segment s; `fence` = issue the release fence first (the
+// notifier batches several segments behind one fence).
+// Default (sys fence): st.release.sys is cumulative -- it orders every store
+// that precedes it in causality order (the consumers' stores via the
+// mbarriers, the producer's edge stores) before the flag.
+// flag_gpu_fence: one fence.acq_rel.gpu, then relaxed system-scope flag
+// stores. Every flag certifies data in the PUBLISHER's own HBM, and peers
+// read it through the publisher's L2; a GPU-scope fence already makes our
+// stores visible there, without the sys fence's wait for the SM's in-flight
+// NVLink traffic (measured 49 us vs 11 us per segment, profiles/README.md).
+__device__ __forceinline__ void publish_flags(const AllreduceArgs& a, const ViewArgs& v,
+                                              const Task& t, int s, uint32_t epoch, bool fence) {
+  const bool up = t.type == 0 && t.parent >= 0;
+  if (!up && t.n_down == 0) return;  // nobody waits for this segment
+  if (fence && a.flag_gpu_fence) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  if (up) {
+    uint32_t* f = &v.peer_ctrl[t.parent]->up[t.color][t.my_slot][s];
+    if (a.flag_gpu_fence) st_relaxed_sys(f, epoch);
+    else st_release_sys(f, epoch);
   } else {
-    for (int c = 0; c < t.n_down; ++c)
-      st_release_sys(&v.peer_ctrl[t.down[c]]->down[t.color][s], epoch);
+    for (int c = 0; c < t.n_down; ++c) {
+      uint32_t* f = &v.peer_ctrl[t.down[c]]->down[t.color][s];
+      if (a.flag_gpu_fence) st_relaxed_sys(f, epoch);
+      else st_release_sys(f, epoch);
+    }
   }
+}
+
+__device__ __forceinline__ void publish(const AllreduceArgs& a, const ViewArgs& v, const Task& t,
+                                        int s, uint32_t epoch) {
+  publish_flags(a, v, t, s, epoch, true);
 }
 
 // ---- optional tracing: %globaltimer events, producer and consumer halves ----
@@ -773,7 +803,7 @@ enum : uint16_t { EV_WAIT0 = 1, EV_WAIT1, EV_ISSUED, EV_FIRST, EV_DONE, EV_PUB, 
 __device__ __forceinline__ void trace_ev(const AllreduceArgs& a, int role, int& n, uint16_t ev,
                                          int seg) {
   if (!a.trace || n >= kTraceHalf) return;
-  TraceEv* e = a.trace + (static_cast<int64_t>(blockIdx.x) * 2 + role) * kTraceHalf + n++;
+  TraceEv* e = a.trace + (static_cast<int64_t>(blockIdx.x) * 3 + role) * kTraceHalf + n++;
   e->t = globaltimer_ns();
   e->cta = blockIdx.x;
   e->ev = ev;
@@ -786,7 +816,8 @@ __device__ __forceinline__ bool aborted(const ViewArgs& v) {
 
 template <int kEpi>
 __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Task& t, int idx,
-                            int m, uint32_t epoch, char* ring, uint64_t* full, uint64_t* empty) {
+                            int m, uint32_t epoch, char* ring, uint64_t* full, uint64_t* empty,
+                            uint64_t* done, uint64_t* ack) {
   const int tid = threadIdx.x;
   const bool final_here = (t.type == 1) || (t.parent < 0);
   const int nrem = t.type == 1 ? 1 : t.n_fold - 1;
@@ -804,7 +835,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         if (mine) item_dispatch<false, kEpi>(a, v, t, final_here, i, i + 1, 0, 1);
       }
       __syncthreads();
-      if (tid == 0 && !(t.type == 0 && t.parent < 0 && t.n_down == 0)) publish(v, t, s, epoch);
+      if (tid == 0 && !(t.type == 0 && t.parent < 0 && t.n_down == 0)) publish(a, v, t, s, epoch);
     }
     return;
   }
@@ -828,7 +859,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         item_dispatch<false, kEpi>(a, v, t, final_here, i, i + 1, 0, 1);
       }
       if (g.nch == 0) {  // nothing for the consumers: release the segment here
-        publish(v, t, s, epoch);
+        publish(a, v, t, s, epoch);
         continue;
       }
       for (int64_t c = 0; c < g.nch; ++c, ++gseq) {
@@ -860,9 +891,56 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
     return;
   }
 
+  if (tid < kConsumerBase) {  // ---------------- notifier warp (lane 0) ----------------
+    if (tid != 32) return;
+    int cn = 0;  // trace events
+    uint32_t j = 0;  // consumer-visible segments seen
+    int pend[kDoneSlots];
+    int npend = 0;
+    for (int s = idx; s < nseg; s += m) {
+      SegGeom g = seg_geom(a, t, s, nrem);
+      if (g.nch == 0) continue;
+      pend[npend++] = s;
+      uint64_t* d = &done[j % kDoneSlots];
+      uint32_t spins = 0;
+      while (!mbar_try_wait(d, (j / kDoneSlots) & 1)) {
+        if ((++spins & 1023) == 0 && aborted(v)) return;
+      }
+      ++j;
+      // batch: also take every following segment that is already finished
+      bool more = true;
+      int s2 = s + m;
+      while (more && npend < kDoneSlots) {
+        if (s2 >= nseg) break;
+        SegGeom g2 = seg_geom(a, t, s2, nrem);
+        if (g2.nch == 0) {
+          s2 += m;
+          continue;
+        }
+        more = mbar_try_wait(&done[j % kDoneSlots], (j / kDoneSlots) & 1);
+        if (more) {
+          pend[npend++] = s2;
+          ++j;
+          s = s2;
+          s2 += m;
+        }
+      }
+      trace_ev(a, 2, cn, EV_DONE, pend[npend - 1]);
+      for (int i = 0; i < npend; ++i) publish_flags(a, v, t, pend[i], epoch, i == 0);
+      trace_ev(a, 2, cn, EV_PUB, pend[npend - 1]);
+      for (int i = 0; i < npend; ++i) {  // free the done slots for the consumers
+        const uint32_t jj = j - npend + i;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&ack[jj % kDoneSlots]))
+                     : "memory");
+      }
+      npend = 0;
+    }
+    return;
+  }
+
   // ---------------- consumer warps ----------------
-  const int ct = tid - 32, nct = kConsumerWarps * 32;
-  uint32_t gseq = 0;
+  const int ct = tid - kConsumerBase, nct = kConsumerWarps * 32;
+  uint32_t gseq = 0, jseg = 0;
   int cn = 0;  // trace events (ct == 0 only)
   for (int s = idx; s < nseg; s += m) {
     SegGeom g = seg_geom(a, t, s, nrem);
@@ -910,13 +988,20 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
       __syncwarp();
       if ((ct & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
     }
-    // all consumer warps are done with segment s: release it
-    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
-    if (ct == 0) {
-      trace_ev(a, 1, cn, EV_DONE, s);
-      publish(v, t, s, epoch);
-      trace_ev(a, 1, cn, EV_PUB, s);
+    // this warp is done with segment s: tell the notifier (the slot must have
+    // been acknowledged for the segment kDoneSlots earlier)
+    if ((ct & 31) == 0) {
+      if (jseg >= kDoneSlots) {
+        uint32_t spins = 0;
+        while (!mbar_try_wait(&ack[jseg % kDoneSlots], ((jseg / kDoneSlots) - 1) & 1)) {
+          if ((++spins & 1023) == 0 && aborted(v)) return;
+        }
+      }
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&done[jseg % kDoneSlots]))
+                   : "memory");
     }
+    __syncwarp();
+    ++jseg;
   }
 }
 
@@ -931,6 +1016,8 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __shared__ uint32_t s_epoch;
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
+  __shared__ __align__(8) uint64_t done[kDoneSlots];
+  __shared__ __align__(8) uint64_t ack[kDoneSlots];
   __shared__ int s_task, s_idx, s_m;
   extern __shared__ __align__(128) char ring[];
   if (tid == 0) {
@@ -938,6 +1025,10 @@ __global__ void __launch_bounds__(kArThreads, 1)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < kDoneSlots; ++s) {
+      mbar_init(&done[s], kConsumerWarps);
+      mbar_init(&ack[s], 1);
     }
     mbar_init_fence();
     int task, idx = 0, m = 1;
@@ -952,7 +1043,7 @@ __global__ void __launch_bounds__(kArThreads, 1)
   int tn = kTraceHalf - 2;  // kernel-level events in the producer half's last slots
   if (tid == 0) trace_ev(a, 0, tn, EV_ENTRY, s_task < 0 ? 0xffff : s_task);
   if (ok && s_task >= 0)
-    run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty);
+    run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty, done, ack);
   __syncthreads();
   if (tid == 0) trace_ev(a, 0, tn, EV_EXIT, s_task < 0 ? 0xffff : s_task);
   exit_barrier(a, v, epoch);
@@ -1443,8 +1534,9 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   a.lag = lag;
   a.max_stage = max_stage;
   a.trace = nullptr;
+  a.flag_gpu_fence = getenv("MD_AR_SYS_FENCE") == nullptr;  // see publish_flags
   if (getenv("MD_AR_TRACE")) {  // diagnostics: one event log per device, per call
-    const size_t bytes = sizeof(TraceEv) * 2 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
+    const size_t bytes = sizeof(TraceEv) * 3 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
     if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
       if (g_trace[dev].ptr) cudaFree(g_trace[dev].ptr);
       MD_CUDA_TRY(cudaMalloc(&g_trace[dev].ptr, bytes));
