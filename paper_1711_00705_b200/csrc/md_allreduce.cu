@@ -301,7 +301,7 @@ __device__ __forceinline__ typename Elem<kVec>::T own_value(const AllreduceArgs&
 // bounded by the ring (3 x 32 KB), not by registers, and the HBM epilogue
 // overlaps the NVLink transfer instead of alternating with it.
 constexpr int kStages = 4;
-constexpr uint32_t kStageBytes = 32 * 1024;
+constexpr uint32_t kStageBytes = 48 * 1024;
 constexpr uint32_t kRingBytes = kStages * kStageBytes;
 
 template <int kEpi>
@@ -731,7 +731,7 @@ struct SegGeom {
 };
 
 __device__ __forceinline__ SegGeom seg_geom(const AllreduceArgs& a, const Task& t, int s,
-                                            int nrem) {
+                                            int nslot) {
   int64_t cstart, clen;
   chunk_of(a.n, a.k, t.color, &cstart, &clen);
   const int64_t A = cstart & ~int64_t(3);
@@ -740,8 +740,8 @@ __device__ __forceinline__ SegGeom seg_geom(const AllreduceArgs& a, const Task& 
   g.hi = min(cstart + clen, A + static_cast<int64_t>(s + 1) * a.seg);
   g.vlo = min(g.hi, (g.lo + 3) & ~int64_t(3));
   g.vhi = max(g.vlo, g.hi & ~int64_t(3));
-  g.C = nrem ? static_cast<int64_t>(kStageBytes / (4u * nrem)) & ~int64_t(3) : 0;
-  g.nch = nrem ? (g.vhi - g.vlo + g.C - 1) / g.C : 0;
+  g.C = nslot ? static_cast<int64_t>(kStageBytes / (4u * nslot)) & ~int64_t(3) : 0;
+  g.nch = nslot ? (g.vhi - g.vlo + g.C - 1) / g.C : 0;
   return g;
 }
 
@@ -840,12 +840,25 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
     return;
   }
 
+  // Every input of a chunk arrives by TMA into one ring stage, laid out as
+  // [remote sources in fold order][own value][W][momentum] (slots of C floats),
+  // so the consumers never wait on a global load: they read SMEM and issue
+  // fire-and-forget stores.
+  const bool tma_own = t.type == 0 && a.n_workers == 0;  // worker folds stay LDG
+  constexpr bool kMomT = kEpi >= 3;
+  const bool tma_epi = kEpi != 0 && final_here;
+  const int own_slot = nrem;
+  const int w_slot = nrem + (tma_own ? 1 : 0);
+  const int m_slot = w_slot + 1;
+  const int nslot = w_slot + (tma_epi ? (kMomT ? 2 : 1) : 0);
+  const int64_t ulen4 = a.update_len & ~int64_t(3);  // W/momentum rows TMA may read
+
   if (tid < 32) {  // ---------------- producer warp (lane 0 works) ----------------
     if (tid != 0) return;
     uint32_t gseq = 0;
     int pn = 0;  // trace events
     for (int s = idx; s < nseg; s += m) {
-      SegGeom g = seg_geom(a, t, s, nrem);
+      SegGeom g = seg_geom(a, t, s, nslot);
       trace_ev(a, 0, pn, EV_WAIT0, s);
       if (!wait_inputs(a, v, t, s, epoch)) return;
       trace_ev(a, 0, pn, EV_WAIT1, s);
@@ -871,9 +884,16 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
           }
         }
         const int64_t clo = g.vlo + c * g.C;
-        const uint32_t bytes = static_cast<uint32_t>((min(g.vhi, clo + g.C) - clo) * 4);
+        const int64_t chi = min(g.vhi, clo + g.C);
+        const uint32_t bytes = static_cast<uint32_t>((chi - clo) * 4);
+        uint32_t wbytes = 0;
+        if (tma_epi) {
+          const int64_t whi = min(chi, ulen4);
+          wbytes = whi > clo ? static_cast<uint32_t>((whi - clo) * 4) : 0u;
+        }
         char* stage = ring + st * kStageBytes;
-        mbar_expect_tx(&full[st], bytes * nrem);
+        const size_t slot = static_cast<size_t>(g.C) * 4;
+        mbar_expect_tx(&full[st], bytes * (nrem + (tma_own ? 1 : 0)) + wbytes * (kMomT ? 2 : 1));
         if (t.type == 1) {
           tma_load_1d(stage, v.peer[t.parent] + clo, bytes, &full[st]);
         } else {
@@ -881,9 +901,14 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
           for (int j = 0; j < t.n_fold; ++j) {
             const int src = t.fold_src[j];
             if (src == v.rank) continue;
-            tma_load_1d(stage + q * g.C * 4, v.peer[src] + clo, bytes, &full[st]);
+            tma_load_1d(stage + q * slot, v.peer[src] + clo, bytes, &full[st]);
             ++q;
           }
+          if (tma_own) tma_load_1d(stage + own_slot * slot, v.buf + clo, bytes, &full[st]);
+        }
+        if (wbytes) {
+          tma_load_1d(stage + w_slot * slot, v.w + clo, wbytes, &full[st]);
+          if (kMomT) tma_load_1d(stage + m_slot * slot, v.mom + clo, wbytes, &full[st]);
         }
       }
       trace_ev(a, 0, pn, EV_ISSUED, s);
@@ -898,32 +923,27 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
     int pend[kDoneSlots];
     int npend = 0;
     for (int s = idx; s < nseg; s += m) {
-      SegGeom g = seg_geom(a, t, s, nrem);
+      SegGeom g = seg_geom(a, t, s, nslot);
       if (g.nch == 0) continue;
       pend[npend++] = s;
-      uint64_t* d = &done[j % kDoneSlots];
       uint32_t spins = 0;
-      while (!mbar_try_wait(d, (j / kDoneSlots) & 1)) {
+      while (!mbar_try_wait(&done[j % kDoneSlots], (j / kDoneSlots) & 1)) {
         if ((++spins & 1023) == 0 && aborted(v)) return;
       }
       ++j;
       // batch: also take every following segment that is already finished
-      bool more = true;
       int s2 = s + m;
-      while (more && npend < kDoneSlots) {
-        if (s2 >= nseg) break;
-        SegGeom g2 = seg_geom(a, t, s2, nrem);
+      while (npend < kDoneSlots && s2 < nseg) {
+        SegGeom g2 = seg_geom(a, t, s2, nslot);
         if (g2.nch == 0) {
           s2 += m;
           continue;
         }
-        more = mbar_try_wait(&done[j % kDoneSlots], (j / kDoneSlots) & 1);
-        if (more) {
-          pend[npend++] = s2;
-          ++j;
-          s = s2;
-          s2 += m;
-        }
+        if (!mbar_try_wait(&done[j % kDoneSlots], (j / kDoneSlots) & 1)) break;
+        pend[npend++] = s2;
+        ++j;
+        s = s2;
+        s2 += m;
       }
       trace_ev(a, 2, cn, EV_DONE, pend[npend - 1]);
       for (int i = 0; i < npend; ++i) publish_flags(a, v, t, pend[i], epoch, i == 0);
@@ -943,8 +963,9 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
   uint32_t gseq = 0, jseg = 0;
   int cn = 0;  // trace events (ct == 0 only)
   for (int s = idx; s < nseg; s += m) {
-    SegGeom g = seg_geom(a, t, s, nrem);
+    SegGeom g = seg_geom(a, t, s, nslot);
     if (g.nch == 0) continue;
+    const size_t slot4 = static_cast<size_t>(g.C) / 4;  // float4 per slot
     for (int64_t c = 0; c < g.nch; ++c, ++gseq) {
       const uint32_t st = gseq % kStages;
       uint32_t spins = 0;
@@ -952,38 +973,49 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         if ((++spins & 1023) == 0 && aborted(v)) return;
       }
       if (c == 0 && ct == 0) trace_ev(a, 1, cn, EV_FIRST, s);
-      const char* stage = ring + st * kStageBytes;
+      const float4* stage = reinterpret_cast<const float4*>(ring + st * kStageBytes);
       const int64_t clo = g.vlo + c * g.C;
       const int64_t chi = min(g.vhi, clo + g.C);
       const int64_t n4 = (chi - clo) / 4;
-      for (int64_t e0 = ct; e0 < n4; e0 += static_cast<int64_t>(kUnroll) * nct) {
-        float4 acc[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t e = e0 + static_cast<int64_t>(u) * nct;
-          if (e >= n4) break;
-          if (t.type == 1) {
-            acc[u] = reinterpret_cast<const float4*>(stage)[e];
-          } else {
-            int q = 0;
-            for (int j = 0; j < t.n_fold; ++j) {
-              float4 x;
-              if (t.fold_src[j] == v.rank) {
-                x = own_value<true>(a, v, clo + 4 * e);
-              } else {
-                x = reinterpret_cast<const float4*>(stage + q * g.C * 4)[e];
-                ++q;
-              }
-              acc[u] = (j == 0) ? x : add4(acc[u], x);
+#pragma unroll 2
+      for (int64_t e = ct; e < n4; e += nct) {
+        const int64_t i = clo + 4 * e;
+        float4 acc;
+        if (t.type == 1) {
+          acc = stage[e];
+        } else {
+          int q = 0;
+          for (int jf = 0; jf < t.n_fold; ++jf) {
+            float4 x;
+            if (t.fold_src[jf] == v.rank) {
+              x = tma_own ? stage[own_slot * slot4 + e] : own_value<true>(a, v, i);
+            } else {
+              x = stage[q * slot4 + e];
+              ++q;
+            }
+            acc = (jf == 0) ? x : add4(acc, x);
+          }
+        }
+        *reinterpret_cast<float4*>(v.buf + i) = acc;
+        if constexpr (kEpi != 0) {
+          if (final_here) {
+            if (i + 4 <= ulen4) {  // W / momentum rows arrived with the chunk
+              float4 w = stage[w_slot * slot4 + e];
+              float4 mm = kMomT ? stage[m_slot * slot4 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+              sgd_elem<kEpi>(w.x, acc.x, mm.x, a);
+              sgd_elem<kEpi>(w.y, acc.y, mm.y, a);
+              sgd_elem<kEpi>(w.z, acc.z, mm.z, a);
+              sgd_elem<kEpi>(w.w, acc.w, mm.w, a);
+              __stcs(reinterpret_cast<float4*>(v.w + i), w);
+              if (kMomT) __stcs(reinterpret_cast<float4*>(v.mom + i), mm);
+            } else {  // the ragged tail of the update range
+              epi_scalar<kEpi>(a, v, i, acc.x);
+              epi_scalar<kEpi>(a, v, i + 1, acc.y);
+              epi_scalar<kEpi>(a, v, i + 2, acc.z);
+              epi_scalar<kEpi>(a, v, i + 3, acc.w);
             }
           }
         }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t e = e0 + static_cast<int64_t>(u) * nct;
-          if (e < n4) *reinterpret_cast<float4*>(v.buf + clo + 4 * e) = acc[u];
-        }
-        if (kEpi != 0 && final_here) epi_batch<true, kEpi>(a, v, clo + 4 * e0, chi, nct, acc);
       }
       __syncwarp();
       if ((ct & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");

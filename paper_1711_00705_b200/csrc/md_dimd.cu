@@ -21,6 +21,8 @@
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -582,6 +584,24 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
   return MD_OK;
 }
 
+// MD_DIMD_TIMING=1: synchronize and print the wall time of each plan phase
+struct PlanTimer {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit PlanTimer(cudaStream_t st) : s(st), on(getenv("MD_DIMD_TIMING") != nullptr) {
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[md_shuffle_plan] %-12s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
                     uint64_t global_rank, int64_t m_segments, const int64_t* n_rec,
                     int32_t* final_member, int64_t* final_rec, int64_t cap, int64_t* n_final,
@@ -609,6 +629,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
   for (int q = S; q <= MD_MAX_GROUP; ++q) tab.base[q] = total;
   cudaStream_t s = as_stream(stream);
   const int64_t m = m_segments;
+  PlanTimer pt(s);
 
   int32_t *dest = nullptr, *flag = nullptr, *excl = nullptr, *got_m = nullptr;
   int64_t *got_r = nullptr, *base_tq = nullptr, *d_nf = nullptr;
@@ -634,6 +655,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
     mine_flag_kernel<<<blocks_for(total), 256, 0, s>>>(dest, total, member, flag);
     MD_LAUNCH_CHECK();
   }
+  pt.mark("dest draws");
   MD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, excl, tot1, s));
   MD_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
   MD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, excl, tot1, s));
@@ -661,6 +683,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
   MD_CUDA_TRY(cudaFreeAsync(seg_bad, s));
   MD_CUDA_TRY(cudaFreeAsync(base_tq, s));
   MD_CUDA_TRY(cudaFreeAsync(d_nf, s));
+  pt.mark("recv order");
 
   // ---- permutation(nf), key _mix64(seed, "perm", global_rank)
   uint64_t parts[3] = {seed, kRolePerm, global_rank};
@@ -698,6 +721,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
       word_base = st_h[1];  // resume at the first unconsumed word
     }
     MD_CUDA_TRY(cudaFreeAsync(ws, s));
+    pt.mark("fy words");
     MD_CUDA_TRY(cudaMallocAsync(&tgt_s, sizeof(uint32_t) * steps, s));
     MD_CUDA_TRY(cudaMallocAsync(&stp, sizeof(uint32_t) * steps, s));
     MD_CUDA_TRY(cudaMallocAsync(&stp_s, sizeof(uint32_t) * steps, s));
@@ -713,6 +737,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
     MD_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, tgt, tgt_s, stp, stp_s,
                                                  static_cast<int>(steps), 0, end_bit, s));
     MD_CUDA_TRY(cudaFreeAsync(tmp, s));
+    pt.mark("fy sort");
     MD_CUDA_TRY(cudaMallocAsync(&nxt, sizeof(int32_t) * nf, s));
     MD_CUDA_TRY(cudaMallocAsync(&parent, sizeof(int32_t) * nf, s));
     MD_CUDA_TRY(cudaMallocAsync(&pa, sizeof(int32_t) * nf, s));
@@ -743,6 +768,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
   }
   MD_CUDA_TRY(cudaFreeAsync(got_m, s));
   MD_CUDA_TRY(cudaFreeAsync(got_r, s));
+  pt.mark("fy resolve");
   *n_final = nf;
   return MD_OK;
 }
