@@ -37,6 +37,7 @@ def main() -> None:
     ap.add_argument("--gathers", type=int, default=1000)
     ap.add_argument("--seed", type=int, default=2017)
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--epochs", type=int, default=3)
     a = ap.parse_args()
 
     import torch
@@ -49,28 +50,34 @@ def main() -> None:
     ep = init_from_env()
     N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
     S, n = N, a.records
-    seed = O.mix64(a.seed, O.SHUF_ROLE, 0)  # epoch 0 key, sgd.py:503-506
+    # epoch keys _mix64(seed, "shuf", epoch), sgd.py:503-506
     with torch.cuda.stream(ep.stream):
         store = dimd.synth_store(n, REC, rank, S, a.seed, 0, S, rank, device=dev)
         torch.cuda.synchronize(dev)
         m_seg = dimd.default_segments(store.nbytes)
-        ep.barrier()
-        t0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(ep.stream)
-        out = dimd.shuffle_all(ep, store, m_segments=m_seg, seed=seed)
-        e1.record(ep.stream)
-        torch.cuda.synchronize(dev)
-        wall = time.perf_counter() - t0
-        ev_ms = e0.elapsed_time(e1)
+        walls, evs, phases_all = [], [], []
+        bad, exact = 0, None
+        for epoch in range(a.epochs):
+            key = O.mix64(a.seed, O.SHUF_ROLE, epoch)
+            ep.barrier()
+            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ep.stream)
+            out = dimd.shuffle_all(ep, store, m_segments=m_seg, seed=key)
+            e1.record(ep.stream)
+            torch.cuda.synchronize(dev)
+            walls.append(time.perf_counter() - t0)
+            evs.append(e0.elapsed_time(e1))
+            phases_all.append(dict(dimd.LAST_SHUFFLE_PHASES))
+            if not a.no_verify:
+                b, gids = dimd.synth_verify(out, a.seed)
+                bad += b
+                if epoch == 0:  # indices: every slot's source vs the oracle's plan
+                    mem, rec = O.shuffle_plan_c(key, 0, S, rank, rank, m_seg, [n] * S)
+                    exact = bool(np.array_equal(gids.cpu().numpy(), mem + S * rec))
+            store = out
+        wall, ev_ms = walls[-1], evs[-1]
         n_out = out.n_records
-        del store
-        torch.cuda.empty_cache()
-        bad, exact = -1, None
-        if not a.no_verify:
-            bad, gids = dimd.synth_verify(out, a.seed)
-            mem, rec = O.shuffle_plan_c(seed, 0, S, rank, rank, m_seg, [n] * S)
-            exact = bool(np.array_equal(gids.cpu().numpy(), mem + S * rec))
         # minibatch gather rate from the new shard
         slots = BatchSlots(32, REC, dev)
         for i in range(20):
@@ -84,8 +91,7 @@ def main() -> None:
         torch.cuda.synchronize(dev)
         slots.check()
         gather_ms = g0.elapsed_time(g1) / a.gathers
-    phases = dict(dimd.LAST_SHUFFLE_PHASES)
-    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases))
+    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases_all, walls))
     if rank == 0:
         wall = max(r[0] for r in rows)
         total = sum(r[2] for r in rows)
@@ -93,6 +99,8 @@ def main() -> None:
         line = {
             "metric": "DIMD shuffle records/s (whole job) and minibatch gather records/s per GPU",
             "n_gpus": N, "records_per_gpu": n, "record_bytes": REC, "m_segments": m_seg,
+            "epochs": a.epochs,
+            "shuffle_s_per_epoch": [max(r[7][e] for r in rows) for e in range(a.epochs)],
             "shuffle_s": wall, "shuffle_records_per_s": total / wall,
             "shuffle_GBps_per_gpu": n * REC / wall / 1e9,
             "nvlink_GBps_per_gpu": nvlink_bytes / wall / 1e9 if S > 1 else None,
@@ -105,7 +113,7 @@ def main() -> None:
             "gather_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
             "gather_hbm_GBps": 2 * 32 * REC / (max(r[5] for r in rows) / 1e3) / 1e9,
         }
-        if rows[0][6]:
+        if rows[0][6] and rows[0][6][-1]:
             line["phases_s_per_rank"] = [r[6] for r in rows]
         print(json.dumps(line), flush=True)
     ep.barrier()

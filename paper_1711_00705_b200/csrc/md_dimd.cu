@@ -224,6 +224,23 @@ __global__ void fy_scan_kernel(const uint32_t* ws, int64_t n_words, int64_t word
     int64_t idx = p - word_base + lane;
     if (p - word_base + 32 > n_words) break;  // need more words
     uint32_t my = ws[idx];
+    // Fast path (no serial dependence): with the same mask for steps s .. s-31,
+    // a lane's word is accepted for sure if v <= s - 31 (at most 31 earlier
+    // lanes can have been accepted) and rejected for sure if v > s. If no lane
+    // falls in between, accepted lane with rank r takes step s - r.
+    if (s >= 64 && mask_of(static_cast<uint32_t>(s - 31)) == mask) {
+      const uint32_t v = my & mask;
+      const bool acc = v <= static_cast<uint32_t>(s - 31);
+      const bool amb = !acc && v <= static_cast<uint32_t>(s);
+      if (!__any_sync(0xffffffffu, amb)) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, acc);
+        if (acc) J[s - __popc(bal & ((1u << lane) - 1u))] = v;
+        s -= __popc(bal);
+        mask = mask_of(static_cast<uint32_t>(s));
+        p += 32;
+        continue;
+      }
+    }
     int used = 32;
     for (int l = 0; l < 32; ++l) {
       uint32_t v = __shfl_sync(0xffffffffu, my, l) & mask;
@@ -630,6 +647,18 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
   cudaStream_t s = as_stream(stream);
   const int64_t m = m_segments;
   PlanTimer pt(s);
+  {  // keep the stream-ordered pool's memory between calls (no re-growth per plan)
+    static std::atomic<uint64_t> pool_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !(pool_set.fetch_or(1ull << dev) & (1ull << dev))) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
+  }
 
   int32_t *dest = nullptr, *flag = nullptr, *excl = nullptr, *got_m = nullptr;
   int64_t *got_r = nullptr, *base_tq = nullptr, *d_nf = nullptr;

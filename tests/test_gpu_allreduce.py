@@ -161,6 +161,47 @@ def test_fused_accumulation_allreduce_and_update(oracle, n, k, arity, mu, wd):
             assert np.array_equal(v, want_v)
 
 
+@pytest.mark.parametrize("case", ["mc_8_10007_4_4", "mc_4_4099_2_4", "mc_16_250_4_4"])
+def test_work_queue_kernel_matches_reference(golden, monkeypatch, case):
+    """The work-queue kernel (fallback when the channel allotment does not
+    fit) folds identically; MD_AR_QUEUE=1 forces it."""
+    monkeypatch.setenv("MD_AR_QUEUE", "1")
+    n, _, k, arity = (int(x) for x in case.split("_")[1:])
+    ts = build_multicolor_trees(n, k, arity)
+    for r in run(n, list(golden[case + "_in"]), "multicolor", tree_set=ts, segment_elems=512):
+        assert np.array_equal(r, golden[case + "_out"])
+
+
+@pytest.mark.parametrize("offset", [1, 2, 3])
+def test_unaligned_buffers_take_the_scalar_path(oracle, offset):
+    """Buffers that are not 16-byte aligned run the work-queue kernel's scalar
+    path (no TMA); bits must not change."""
+    n, P = 4, 10_007
+    rng = np.random.default_rng(offset)
+    arrays = [rng.standard_normal(P).astype(np.float32) for _ in range(n)]
+    w0 = rng.standard_normal(P).astype(np.float32)
+    tables = oracle.tables_from_trees(n, oracle.trees(n, 4, 4))
+    g = oracle.fold_c(tables, arrays)
+    want_w, _ = oracle.sgd_np(w0, g, None, 1e-3, 0.0, 0.0)
+    ts = build_multicolor_trees(n, 4, 4)
+
+    def prog(ep):
+        dev = ep.torch_device
+        base = torch.zeros(P + offset, device=dev)
+        view = base[offset:]
+        view.copy_(torch.from_numpy(arrays[ep.rank]))
+        wb = torch.zeros(P + offset, device=dev)
+        w = wb[offset:]
+        w.copy_(torch.from_numpy(w0))
+        allreduce(ep, GradientBuffer(view), "multicolor", tree_set=ts, segment_elems=1000,
+                  update=SgdUpdate(weights=w, c=1e-3))
+        return view.cpu().numpy(), w.cpu().numpy()
+
+    for gb, w in run_ranks(n, "cuda", prog, emulate=True).results:
+        assert np.array_equal(gb, g)
+        assert np.array_equal(w, want_w)
+
+
 @pytest.mark.parametrize("workers", [0, 2])
 @pytest.mark.parametrize("mu,wd", [(0.0, 0.0), (0.9, 1e-4)])
 def test_single_rank_fused_update(oracle, workers, mu, wd):
