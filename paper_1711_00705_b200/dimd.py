@@ -421,6 +421,52 @@ def group_record_counts(channel, members, n_records: int, m_segments: int) -> li
 LAST_SHUFFLE_PHASES: dict[str, float] = {}
 
 
+class _ShardArena:
+    """Reusable output blobs for successive shuffles of one endpoint.
+
+    Peers map a shard's blob through CUDA IPC (md_mem_import), and mapping a
+    24 GB allocation costs tens of ms; reusing the same few allocations makes
+    the mappings hits of the per-process import cache after the first epochs.
+    A slot is reused only when the ShardStore that owned it has been garbage
+    collected, so no live store is ever overwritten."""
+
+    HEADROOM = 1.03
+
+    def __init__(self):
+        self.slots: list[list] = []  # [tensor, weakref to owning store or None]
+
+    def take(self, nbytes: int, device) -> tuple[torch.Tensor, list]:
+        import weakref  # noqa: F401
+
+        free = [s for s in self.slots if s[1] is None or s[1]() is None]
+        for s in sorted(free, key=lambda s: s[0].numel()):
+            if s[0].numel() >= nbytes:
+                return s[0][: max(1, nbytes)], s
+        if free:  # grow the largest free slot
+            slot = max(free, key=lambda s: s[0].numel())
+            slot[0] = None
+        else:
+            slot = [None, None]
+            self.slots.append(slot)
+        slot[0] = torch.empty(max(1, int(nbytes * self.HEADROOM)), dtype=torch.uint8,
+                              device=device)
+        return slot[0][: max(1, nbytes)], slot
+
+    @staticmethod
+    def bind(slot: list, store) -> None:
+        import weakref
+
+        slot[1] = weakref.ref(store)
+
+
+def _arena(ep) -> _ShardArena:
+    ar = getattr(ep, "_shard_arena", None)
+    if ar is None:
+        ar = _ShardArena()
+        ep._shard_arena = ar
+    return ar
+
+
 class _PhaseClock:
     """Host wall time per shuffle phase (MD_DIMD_TIMING=1: synchronizes
     between phases and records into LAST_SHUFFLE_PHASES)."""
@@ -493,7 +539,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
         )
     )
     mark("index")
-    blob = torch.empty(max(1, int(total.value)), dtype=torch.uint8, device=dev)
+    blob, slot = _arena(ep).take(int(total.value), dev)
     _lib.check(
         lib.md_shuffle_pull(
             S, _lib.ptr_array([v_blob.ptrs[m] for m in members]),
@@ -508,6 +554,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     out = ShardStore(blob, off[:n_final], ln[:n_final], lb[:n_final], store.group_id, S,
                      store.rank_in_group)
     out._nbytes = int(total.value)
+    _ShardArena.bind(slot, out)
     return out
 
 
