@@ -25,7 +25,9 @@ def pytest_configure(config):
 
 @pytest.fixture(scope="session")
 def golden():
-    return np.load(ROOT / "tests" / "golden" / "golden.npz")
+    # eager dict: the lazy NpzFile is not safe to read from rank threads
+    with np.load(ROOT / "tests" / "golden" / "golden.npz") as z:
+        return {k: z[k] for k in z.files}
 
 
 @pytest.fixture(scope="session")
