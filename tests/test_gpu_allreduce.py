@@ -278,6 +278,34 @@ def test_closed_form_check_of_reference_bench_fill(oracle):
 
 @pytest.mark.multigpu
 @need_gpus(2)
+def test_lost_peer_surfaces_as_not_exposed():
+    """A rank that never enters the collective must not hang its peer: the
+    device watchdog ends the wait (transport/base.py:28 semantics) and the
+    waiting rank raises NotExposed."""
+    import time
+
+    from paper_1711_00705_b200.transport import PeerView
+
+    def prog(ep):
+        if ep.rank == 1:
+            return None  # never enters the collective
+        buf = GradientBuffer(torch.ones(1024, device=ep.torch_device))
+        # pre-registered view, so the host-side registration (which would fail
+        # fast) is skipped and the DEVICE wait is what must time out
+        buf.peers = (ep, PeerView([buf.data.data_ptr()] * ep.n_ranks, 4096, buf.data))
+        t0 = time.perf_counter()
+        try:
+            allreduce(ep, buf, "multicolor", tree_set=build_multicolor_trees(2, 1, 4))
+        except errors.NotExposed:
+            return time.perf_counter() - t0
+        return -1.0
+
+    waited = run_ranks(2, "cuda", prog, emulate=False, pull_timeout=2.0).results[0]
+    assert waited is not None and 1.5 < waited < 20.0, waited
+
+
+@pytest.mark.multigpu
+@need_gpus(2)
 @pytest.mark.parametrize("n,L,k,arity", [(2, 4099, 1, 4), (2, 4099, 2, 4), (2, 0, 2, 4)])
 def test_p2p_two_gpus_match_reference(golden, n, L, k, arity):
     inp = golden[f"mc_{n}_{L}_{k}_{arity}_in"]
