@@ -1630,11 +1630,17 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     a.trace = static_cast<TraceEv*>(g_trace[dev].ptr);
   }
   void* args[] = {&a};
-  // cooperative launch: every CTA (of every emulated rank) co-resident, so
-  // flag waits between CTAs can never deadlock on scheduling
-  MD_CUDA_TRY(cudaLaunchCooperativeKernel(kern,
-                                          dim3(ctas * n_views), dim3(kArThreads), args,
-                                          kRingBytes, as_stream(stream)));
+  // Emulated ranks wait on each other's CTAs on ONE device: a cooperative
+  // launch guarantees they are co-resident. A real rank's CTAs only wait on
+  // other GPUs (never on a sibling CTA), so a plain launch of <= one CTA per
+  // SM is deadlock-free there; MD_AR_COOP=1 forces the cooperative launch.
+  if (n_views > 1 || getenv("MD_AR_COOP")) {
+    MD_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(ctas * n_views), dim3(kArThreads), args,
+                                            kRingBytes, as_stream(stream)));
+  } else {
+    MD_CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(kArThreads), args, kRingBytes,
+                                 as_stream(stream)));
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return MD_OK;
 }

@@ -56,7 +56,9 @@ def analyse(path: str) -> dict:
         g["idle_tail_us"].append(
             (exit_ - max((t for t, e, s in evs if e in ("DONE", "PUB", "ISSUED")), default=exit_)) / 1e3
         )
-    summary = {"kernel_us": (max(e for _, e in spans) - min(s for s, _ in spans)) / 1e3}
+    summary = {"kernel_us": (max(e for _, e in spans) - min(s for s, _ in spans)) / 1e3,
+               "entry_spread_us": (max(s for s, _ in spans) - min(s for s, _ in spans)) / 1e3,
+               "first_entry_to_last_exit_us": (max(e for _, e in spans) - min(s for s, _ in spans)) / 1e3}
     for task, g in sorted(out.items()):
         summary[f"task{task}"] = {
             k: (round(float(np.mean(v)), 2), round(float(np.sum(v)), 1), len(v))
@@ -69,6 +71,7 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--seg", type=int, default=0)
     ap.add_argument("--plain", action="store_true")
+    ap.add_argument("--elems", type=int, default=25_600_000)
     ap.add_argument("--out", default="gpurun_out")
     a = ap.parse_args()
     import torch
@@ -81,7 +84,7 @@ def main() -> None:
     ep = init_from_env()
     N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
     lib = _lib.load()
-    P = 25_600_000
+    P = a.elems
     ts, _ = comm_plan(N, "multicolor")
     grad = GradientBuffer.alloc(P + 2, ep)
     w = torch.zeros(P, device=dev)
