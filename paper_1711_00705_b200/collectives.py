@@ -440,11 +440,12 @@ def alltoallv(ep, send: VarPayload) -> VarPayload:
     source's registered send buffer (NVLink reads)."""
     send.validate(ep.n_ranks)
     host = not isinstance(send.data, torch.Tensor)
-    src = (
-        torch.frombuffer(bytearray(send.data), dtype=torch.uint8).to(ep.torch_device)
-        if host
-        else send.data
-    )
+    if host:
+        raw = bytearray(send.data)
+        src = (torch.frombuffer(raw, dtype=torch.uint8).to(ep.torch_device) if raw
+               else torch.zeros(1, dtype=torch.uint8, device=ep.torch_device))
+    else:
+        src = send.data
     if src.numel() == 0:
         src = torch.zeros(1, dtype=torch.uint8, device=ep.torch_device)
     torch.cuda.current_stream(ep.torch_device).synchronize()
