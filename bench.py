@@ -66,6 +66,7 @@ def args_():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly")
     return ap.parse_args()
 
 
@@ -147,7 +148,7 @@ def run_ours(a) -> None:
 
     from paper_1711_00705_b200 import _lib, dimd
     from paper_1711_00705_b200.collectives import GradientBuffer, SgdUpdate, allreduce
-    from paper_1711_00705_b200.dimd import BatchRequest, BatchSlots, random_batch_device
+    from paper_1711_00705_b200.dimd import BatchRequest, BatchSlots, BatchStream, random_batch_device, random_batch_picks
     from paper_1711_00705_b200.sgd import (
         SAMPLE_ROLE, DeviceModel, TrainConfig, check_replicas, lr_at, lr_schedule)
     from paper_1711_00705_b200.transport import init_from_env
@@ -173,6 +174,7 @@ def run_ours(a) -> None:
         model = DeviceModel(w, torch.zeros_like(w))
         grad = GradientBuffer.alloc(P + 2, ep)
         slots = BatchSlots(BATCH, REC, dev)
+        batches = BatchStream(store, BATCH, REC, SEED, SAMPLE_ROLE, rank)  # device step counter
         upd = SgdUpdate(weights=model.weights, c=lr / B, momentum=model.momentum, mu=MOM,
                         wd_b=WD * B, update_len=P)
     torch.cuda.synchronize(dev)
@@ -182,12 +184,12 @@ def run_ours(a) -> None:
 
     ar_ev = []
 
-    def step(i, timed=False):
-        key = dimd._mix64(SEED, SAMPLE_ROLE, rank, i)
-        random_batch_device(store, BatchRequest(BATCH, key), REC, slots)
+    def step(timed=False):
+        batches.next()  # picks for step i = the stream's device counter, then the gather
         fill()
-        if timed:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if timed:  # external: the pair also works as event nodes inside a captured graph
+            e0 = torch.cuda.Event(enable_timing=True, external=True)
+            e1 = torch.cuda.Event(enable_timing=True, external=True)
             e0.record(stream)
         allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
         if timed:
@@ -197,9 +199,13 @@ def run_ours(a) -> None:
     with torch.cuda.stream(stream):
         # correctness before timing (reference bench.py:198-212 + 258-268):
         # closed-form f64 sum of the fill, rel err <= 1e-5
-        step(0)
+        step()
         ep.synchronize()
-        slots.check()
+        batches.slots.check()
+        key0 = dimd._mix64(SEED, SAMPLE_ROLE, rank, 0)
+        want_picks = random_batch_picks(store, BatchRequest(BATCH, key0))
+        if not torch.equal(batches.slots.picks, want_picks):
+            raise SystemExit("device-keyed batch stream diverged from random_batch")
         idx = np.arange(0, P, 7919)
         got = grad.data[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
         total = sum((r + 1) * np.pi / N for r in range(N))
@@ -207,9 +213,23 @@ def run_ours(a) -> None:
         rel = float(np.max(np.abs(got - want) / np.abs(want)))
         if rel > 1e-5:
             raise SystemExit(f"allreduce result check failed: max rel err {rel:.3g}")
-        for i in range(1, a.warmup + 1):
-            step(i)
+        for _ in range(a.warmup):
+            step()
         ep.synchronize()
+        graph = None
+        if not a.no_graph:
+            # the K timed steps as ONE CUDA graph: every kernel (picks, gather,
+            # fill, fused allreduce) is replay-safe -- step keys and allreduce
+            # epochs are device counters -- so replays need no host work
+            l0 = lib.md_launch_count()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
+                for _ in range(a.steps):
+                    step(timed=True)
+            captured = lib.md_launch_count() - l0
+            ep.barrier()
+            graph.replay()  # upload + one more warm pass of the same work
+            ep.synchronize()
 
         # the sampler starts (and finishes initialising) before the barrier so
         # every rank leaves the barrier together
@@ -221,15 +241,18 @@ def run_ours(a) -> None:
         l0 = lib.md_launch_count()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for i in range(a.steps):
-            step(a.warmup + 1 + i, timed=True)
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(a.steps):
+                step(timed=True)
         t1.record(stream)
         torch.cuda.synchronize(dev)
-        launches = lib.md_launch_count() - l0
+        launches = captured if graph is not None else lib.md_launch_count() - l0
         ep.barrier()
         clk = clocks.stop() if clocks else None
         ep.take_error()
-        slots.check()
+        batches.slots.check()
         ms = t0.elapsed_time(t1)
         ar_ms = sum(e0.elapsed_time(e1) for e0, e1 in ar_ev) / len(ar_ev)
         if os.environ.get("MD_BENCH_DEBUG"):
@@ -341,6 +364,7 @@ def run_ours(a) -> None:
             "shard_records_per_gpu": SHARD, "params": P, "algo": "multicolor",
             "k_colors": ts.k if ts else 1, "arity": ts.arity if ts else None,
             "parallelism": f"dp{N}",
+            "cuda_graph": not a.no_graph,
             "l2": "inputs larger than L2 (W + momentum + gradient = 307 MB per GPU)",
         },
         "allreduce": {"ms": ar_ms, "bus_gbps": bus,

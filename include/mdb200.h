@@ -154,6 +154,13 @@ uint64_t md_mix64(const uint64_t* parts, int32_t n);
  * (numpy Philox4x64-10 stream, 32-bit Lemire with rejection). Device output. */
 int md_random_batch(uint64_t key, int64_t n_records, int64_t batch, int64_t* picks, void* stream);
 
+/* Graph-replayable random_batch for a training loop: the key is
+ * _mix64(seed, role, worker, *step) computed on device (sgd.py:303-307) and
+ * *step (device int64) is incremented by the kernel, so a captured CUDA graph
+ * draws the next step's batch on every replay. batch <= 1024. */
+int md_random_batch_step(uint64_t seed, uint64_t role, uint64_t worker, int64_t* step,
+                         int64_t n_records, int64_t batch, int64_t* picks, void* stream);
+
 /* Gather records picks[0..batch) of a shard (blob + index off/len/label) into
  * `out`: fixed stride when out_stride > 0 (every picked record must be exactly
  * out_stride bytes, else MD_ERR_LENGTH_MISMATCH), packed at out_off[i]

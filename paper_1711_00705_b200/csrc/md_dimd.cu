@@ -89,6 +89,27 @@ __global__ void __launch_bounds__(1024) picks_block_kernel(uint64_t key, uint32_
   if (__syncthreads_or(rejected) && i == 0)  // rare: redo the whole stream serially
     lemire_serial(key, static_cast<uint64_t>(batch), n, nullptr, picks);
 }
+// Graph-replayable variant: key from a device step counter, which it advances.
+__global__ void __launch_bounds__(1024) picks_step_kernel(uint64_t seed, uint64_t role,
+                                                          uint64_t worker, int64_t* step,
+                                                          uint32_t n, int64_t batch,
+                                                          int64_t* picks) {
+  const int64_t st = *step;
+  const uint64_t key =
+      mix64_step(mix64_step(mix64_step(mix64_step(0, seed), role), worker),
+                 static_cast<uint64_t>(st));
+  const int i = threadIdx.x;
+  int rejected = 0;
+  if (i < batch) {
+    uint32_t v = 0;
+    if (n == 1) picks[i] = 0;
+    else if (lemire_fast(key, static_cast<uint64_t>(i), n, &v)) picks[i] = v;
+    else rejected = 1;
+  }
+  if (__syncthreads_or(rejected) && i == 0)
+    lemire_serial(key, static_cast<uint64_t>(batch), n, nullptr, picks);
+  if (i == 0) *step = st + 1;  // every thread read *step before the barrier above
+}
 __global__ void picks_serial_kernel(uint64_t key, uint32_t n, int64_t batch, int64_t* picks,
                                     const int* bad) {
   if (*bad) lemire_serial(key, static_cast<uint64_t>(batch), n, nullptr, picks);
@@ -582,6 +603,22 @@ int md_random_batch(uint64_t key, int64_t n_records, int64_t batch, int64_t* pic
     MD_LAUNCH_CHECK();
   }
   MD_CUDA_TRY(cudaFreeAsync(bad, s));
+  return MD_OK;
+}
+
+int md_random_batch_step(uint64_t seed, uint64_t role, uint64_t worker, int64_t* step,
+                         int64_t n_records, int64_t batch, int64_t* picks, void* stream) {
+  if (n_records <= 0) {
+    set_error("cannot sample from an empty shard");
+    return MD_ERR_EMPTY_SHARD;
+  }
+  if (batch < 1 || batch > 1024 || n_records > 0xFFFFFFFFLL) {
+    set_error("md_random_batch_step needs 1 <= batch <= 1024 and < 2^32 records");
+    return MD_ERR_INVALID_CONFIG;
+  }
+  picks_step_kernel<<<1, 1024, 0, as_stream(stream)>>>(
+      seed, role, worker, step, static_cast<uint32_t>(n_records), batch, picks);
+  MD_LAUNCH_CHECK();
   return MD_OK;
 }
 

@@ -319,17 +319,54 @@ def random_batch_device(store: ShardStore, req: BatchRequest, record_bytes: int 
     if own:
         slots = BatchSlots(B, record_bytes, store.device)
     random_batch_picks(store, req, slots.picks)
+    _gather_fixed(store, slots, B, record_bytes)
+    if own:
+        slots.check()
+    return slots.records, slots.labels, slots.picks
+
+
+def _gather_fixed(store: ShardStore, slots: BatchSlots, batch: int, record_bytes: int) -> None:
     _lib.check(
         _lib.load().md_gather(
             store.blob.data_ptr(), store.off.data_ptr(), store.length.data_ptr(),
-            store.label.data_ptr(), slots.picks.data_ptr(), B, slots.records.data_ptr(),
+            store.label.data_ptr(), slots.picks.data_ptr(), batch, slots.records.data_ptr(),
             record_bytes, None, slots.labels.data_ptr(), slots.err.data_ptr(),
             _stream(store.device),
         )
     )
-    if own:
-        slots.check()
-    return slots.records, slots.labels, slots.picks
+
+
+class BatchStream:
+    """One worker's per-step minibatches as a graph-replayable pair of kernels.
+
+    ``next()`` draws the batch of the current step with the key
+    ``_mix64(seed, role, worker, step)`` -- the key sgd.sample_node_batch uses
+    (reference sgd.py:303-307) -- gathers it into ``slots`` and advances the
+    step counter, which lives on the device: a CUDA graph that captured one
+    ``next()`` draws a fresh, bit-identical-to-the-reference batch on every
+    replay. Fixed-size records only (as ``random_batch_device``), batch <= 1024."""
+
+    def __init__(self, store: ShardStore, batch: int, record_bytes: int, seed: int, role: int,
+                 worker: int, start_step: int = 0):
+        if store.n_records == 0:
+            raise EmptyShard("cannot sample from an empty shard")
+        if not 1 <= batch <= 1024:
+            raise InvalidConfig(f"BatchStream batch must be in [1, 1024], got {batch}")
+        self.store, self.batch, self.record_bytes = store, batch, record_bytes
+        self.seed, self.role, self.worker = seed & _MASK64, role & _MASK64, worker & _MASK64
+        self.step = torch.full((1,), start_step, dtype=torch.int64, device=store.device)
+        self.slots = BatchSlots(batch, record_bytes, store.device)
+
+    def next(self):
+        st = self.store
+        _lib.check(
+            _lib.load().md_random_batch_step(
+                self.seed, self.role, self.worker, self.step.data_ptr(), st.n_records, self.batch,
+                self.slots.picks.data_ptr(), _stream(st.device),
+            )
+        )
+        _gather_fixed(st, self.slots, self.batch, self.record_bytes)
+        return self.slots.records, self.slots.labels, self.slots.picks
 
 
 def random_batch(store: ShardStore, req: BatchRequest) -> list[Record]:

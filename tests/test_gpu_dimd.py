@@ -148,3 +148,37 @@ def test_exchange_moves_every_byte(oracle):
     for r, (_, g) in enumerate(res):
         wm, wr = oracle.shuffle_plan_c(77, 0, S, r, r, 3, [n_local] * S)
         assert np.array_equal(g, wm + S * wr)
+
+
+def test_batch_stream_matches_keyed_batches_eager_and_graph():
+    """BatchStream (device step counter) draws exactly sample_node_batch's
+    per-step batches, eagerly and from replays of one captured CUDA graph."""
+    from paper_1711_00705_b200.dimd import BatchRequest, BatchStream, _mix64, random_batch_device
+    from paper_1711_00705_b200.sgd import SAMPLE_ROLE
+
+    dev = torch.device("cuda", 0)
+    store = dimd.synth_store(5000, 96, 0, 1, 7, 0, 1, 0, device=dev)
+    bs = BatchStream(store, 32, 96, 7, SAMPLE_ROLE, 3, start_step=5)
+
+    def want(step):
+        recs, labels, picks = random_batch_device(store, BatchRequest(32, _mix64(7, SAMPLE_ROLE, 3, step)), 96)
+        return recs.clone(), labels.clone(), picks.clone()
+
+    for step in (5, 6):
+        got = [t.clone() for t in bs.next()]
+        for g, w in zip(got, want(step)):
+            assert torch.equal(g, w)
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        bs.next()
+    assert int(bs.step.item()) == 7  # capture does not execute
+    for step in (7, 8, 9):
+        graph.replay()
+        torch.cuda.synchronize(dev)
+        for g, w in zip((bs.slots.records, bs.slots.labels, bs.slots.picks), want(step)):
+            assert torch.equal(g, w)
+    bs.slots.check()
+    with pytest.raises(errors.InvalidConfig):
+        BatchStream(store, 2000, 96, 7, SAMPLE_ROLE, 0)
