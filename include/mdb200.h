@@ -154,6 +154,10 @@ uint64_t md_mix64(const uint64_t* parts, int32_t n);
  * (numpy Philox4x64-10 stream, 32-bit Lemire with rejection). Device output. */
 int md_random_batch(uint64_t key, int64_t n_records, int64_t batch, int64_t* picks, void* stream);
 
+/* Diagnostics: a one-thread kernel that writes %globaltimer (ns) to *dst when
+ * it runs on `stream` (brackets a call on the device's own clock). */
+int md_stamp(uint64_t* dst, void* stream);
+
 /* Graph-replayable random_batch for a training loop: the key is
  * _mix64(seed, role, worker, *step) computed on device (sgd.py:303-307) and
  * *step (device int64) is incremented by the kernel, so a captured CUDA graph

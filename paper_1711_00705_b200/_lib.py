@@ -63,6 +63,7 @@ SIGNATURES = {
     "md_trace_dump": (C.c_int, [_i32, C.c_char_p]),
     "md_mix64": (_u64, [C.POINTER(_u64), _i32]),
     "md_random_batch": (C.c_int, [_u64, _i64, _i64, _vp, _vp]),
+    "md_stamp": (C.c_int, [_vp, _vp]),
     "md_random_batch_step": (C.c_int, [_u64, _u64, _u64, _vp, _i64, _i64, _vp, _vp]),
     "md_gather": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
     "md_shuffle_plan": (

@@ -521,6 +521,21 @@ __device__ __forceinline__ void item_dispatch(const AllreduceArgs& a, const View
   if (kEpi != 0 && final_here) epilogue_pass<kVec, kEpi>(a, v, lo, hi, tid, nthr);
 }
 
+// ---- optional tracing: %globaltimer events, producer and consumer halves ----
+constexpr int kTraceHalf = 512;  // events per CTA per role
+enum : uint16_t { EV_WAIT0 = 1, EV_WAIT1, EV_ISSUED, EV_FIRST, EV_DONE, EV_PUB, EV_ENTRY, EV_EXIT,
+                  EV_START, EV_LEFT, EV_X1, EV_X2 };
+
+__device__ __forceinline__ void trace_ev(const AllreduceArgs& a, int role, int& n, uint16_t ev,
+                                         int seg) {
+  if (!a.trace || n >= kTraceHalf) return;
+  TraceEv* e = a.trace + (static_cast<int64_t>(blockIdx.x) * 3 + role) * kTraceHalf + n++;
+  e->t = globaltimer_ns();
+  e->cta = blockIdx.x;
+  e->ev = ev;
+  e->seg = static_cast<uint16_t>(seg);
+}
+
 // Entry barrier + length agreement. Returns false if this view must skip work.
 __device__ bool entry_barrier(const AllreduceArgs& a, const ViewArgs& v, int local_cta,
                               uint32_t epoch) {
@@ -556,23 +571,42 @@ __device__ bool entry_barrier(const AllreduceArgs& a, const ViewArgs& v, int loc
   return s_ok != 0;
 }
 
+// The done flag only certifies "every read this rank made of your memory has
+// completed": those reads were consumed (TMA completion / register use)
+// before the CTA got here, and every datum a peer reads from us was already
+// released by its segment flag. So (flag_gpu_fence) a GPU-scope acq_rel
+// counter orders the CTAs and relaxed system-scope stores carry the flag --
+// the two sys fences this replaces cost ~5 us per call (profiles/README.md).
 __device__ void exit_barrier(const AllreduceArgs& a, const ViewArgs& v, uint32_t epoch) {
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
-    uint32_t prev = atomicAdd(&v.ctrl->finished, 1u);
+    uint32_t prev;
+    if (a.flag_gpu_fence) {
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "l"(&v.ctrl->finished) : "memory");
+    } else {
+      __threadfence_system();
+      prev = atomicAdd(&v.ctrl->finished, 1u);
+    }
     s_last = (prev == static_cast<uint32_t>(a.ctas_per_view - 1));
   }
   __syncthreads();
   if (!s_last) return;
   // last CTA of this rank: nobody here reads peer memory any more
   const int tid = threadIdx.x;
+  int tn = kTraceHalf - 6;
+  if (tid == 0) trace_ev(a, 0, tn, EV_X1, 0);
   if (tid < a.n_ranks && tid != v.rank) {
-    __threadfence_system();
-    st_release_sys(&v.peer_ctrl[tid]->done_epoch[v.rank], epoch);
+    if (a.flag_gpu_fence) {
+      st_relaxed_sys(&v.peer_ctrl[tid]->done_epoch[v.rank], epoch);
+    } else {
+      __threadfence_system();
+      st_release_sys(&v.peer_ctrl[tid]->done_epoch[v.rank], epoch);
+    }
   }
   __syncthreads();
+  if (tid == 0) trace_ev(a, 0, tn, EV_X2, 0);
   if (tid == 0) {
     for (int r = 0; r < a.n_ranks; ++r) {
       if (r == v.rank) continue;
@@ -804,10 +838,6 @@ __device__ bool wait_inputs(const AllreduceArgs& a, const ViewArgs& v, const Tas
 }
 
 // Release segment s: up flag in the parent, or down flags in the children.
-__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // Flag stores of segment s; `fence` = issue the release fence first (the
 // notifier batches several segments behind one fence).
 // Default (sys fence): st.release.sys is cumulative -- it orders every store
@@ -839,20 +869,6 @@ __device__ __forceinline__ void publish_flags(const AllreduceArgs& a, const View
 __device__ __forceinline__ void publish(const AllreduceArgs& a, const ViewArgs& v, const Task& t,
                                         int s, uint32_t epoch) {
   publish_flags(a, v, t, s, epoch, true);
-}
-
-// ---- optional tracing: %globaltimer events, producer and consumer halves ----
-constexpr int kTraceHalf = 512;  // events per CTA per role
-enum : uint16_t { EV_WAIT0 = 1, EV_WAIT1, EV_ISSUED, EV_FIRST, EV_DONE, EV_PUB, EV_ENTRY, EV_EXIT };
-
-__device__ __forceinline__ void trace_ev(const AllreduceArgs& a, int role, int& n, uint16_t ev,
-                                         int seg) {
-  if (!a.trace || n >= kTraceHalf) return;
-  TraceEv* e = a.trace + (static_cast<int64_t>(blockIdx.x) * 3 + role) * kTraceHalf + n++;
-  e->t = globaltimer_ns();
-  e->cta = blockIdx.x;
-  e->ev = ev;
-  e->seg = static_cast<uint16_t>(seg);
 }
 
 __device__ __forceinline__ bool aborted(const ViewArgs& v) {
@@ -1122,14 +1138,16 @@ __global__ void __launch_bounds__(kArThreads, 1)
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
+  int tn = kTraceHalf - 4;  // kernel-level events in the producer half's last slots
+  if (tid == 0) trace_ev(a, 0, tn, EV_START, s_task < 0 ? 0xffff : s_task);
   const bool ok = entry_barrier(a, v, local_cta, epoch);
-  int tn = kTraceHalf - 2;  // kernel-level events in the producer half's last slots
   if (tid == 0) trace_ev(a, 0, tn, EV_ENTRY, s_task < 0 ? 0xffff : s_task);
   if (ok && s_task >= 0)
     run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty, done, ack);
   __syncthreads();
   if (tid == 0) trace_ev(a, 0, tn, EV_EXIT, s_task < 0 ? 0xffff : s_task);
   exit_barrier(a, v, epoch);
+  if (tid == 0) trace_ev(a, 0, tn, EV_LEFT, s_task < 0 ? 0xffff : s_task);
 }
 
 struct TraceBuf {
@@ -1623,9 +1641,10 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
       if (g_trace[dev].ptr) cudaFree(g_trace[dev].ptr);
       MD_CUDA_TRY(cudaMalloc(&g_trace[dev].ptr, bytes));
+      MD_CUDA_TRY(cudaMemset(g_trace[dev].ptr, 0, bytes));
       g_trace[dev].bytes = bytes;
     }
-    MD_CUDA_TRY(cudaMemsetAsync(g_trace[dev].ptr, 0, bytes, as_stream(stream)));
+    // (md_trace_dump re-zeroes the log, so a traced call adds no work of its own)
     g_trace[dev].used = bytes;
     a.trace = static_cast<TraceEv*>(g_trace[dev].ptr);
   }
@@ -1657,6 +1676,7 @@ extern "C" int md_trace_dump(int32_t device, const char* path) {
   MD_CUDA_TRY(cudaGetDevice(&prev));
   MD_CUDA_TRY(cudaSetDevice(device));
   cudaError_t e = cudaMemcpy(host.data(), g_trace[device].ptr, host.size(), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(g_trace[device].ptr, 0, g_trace[device].bytes);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     set_error("trace copy: %s", cudaGetErrorString(e));
