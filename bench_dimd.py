@@ -12,8 +12,8 @@ default_segments(shard bytes), as the reference computes it) are timed (wall,
 max over ranks; steady state = median of epochs >= 3). After every epoch each
 record is verified against the generator; after the first, every slot's
 source index is compared with the CPU oracle's plan (numpy-Philox semantics)
--- bit-exact indices. Then 1000
-minibatch gathers of 32 records are timed. Prints one JSON line.
+-- bit-exact indices. Then the training loop's 32-record batches (CUDA-graph
+replays of BatchStream.next()) and one bulk gather are timed. Prints one JSON line.
 Roofline: the exchange must move (S-1)/S of the shard bytes over NVLink
 (pull) and write every byte once into HBM.
 """
@@ -33,10 +33,19 @@ sys.path.insert(0, str(ROOT))
 REC = 224 * 224 * 3
 
 
+def _hbm_peak():
+    try:
+        from bench import hbm_peak
+        return hbm_peak()
+    except Exception:
+        return None
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--records", type=int, default=160_000)
     ap.add_argument("--gathers", type=int, default=1000)
+    ap.add_argument("--bulk", type=int, default=8192, help="records in the bulk-gather probe")
     ap.add_argument("--seed", type=int, default=2017)
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--epochs", type=int, default=5)
@@ -47,6 +56,7 @@ def main() -> None:
     from oracle import oracle as O
     from paper_1711_00705_b200 import dimd
     from paper_1711_00705_b200.dimd import BatchRequest, BatchSlots, random_batch_device
+    from paper_1711_00705_b200.sgd import SAMPLE_ROLE
     from paper_1711_00705_b200.transport import init_from_env
 
     ep = init_from_env()
@@ -82,20 +92,42 @@ def main() -> None:
         # peers' shard allocations (cached afterwards, dimd._ShardArena)
         wall, ev_ms = float(np.median(walls[2:] if len(walls) > 2 else walls)), evs[-1]
         n_out = out.n_records
-        # minibatch gather rate from the new shard
-        slots = BatchSlots(32, REC, dev)
-        for i in range(20):
-            random_batch_device(out, BatchRequest(32, i), REC, slots)
+        # minibatch gathers from the new shard. (1) the training loop's
+        # 32-record batches: BatchStream.next() (device-keyed picks + gather)
+        # captured 100x into one CUDA graph, replayed -- device time per batch,
+        # no host work in between; (2) one bulk gather of --bulk records for
+        # the kernel's HBM roofline (read + write of every record byte).
+        bs = dimd.BatchStream(out, 32, REC, a.seed, SAMPLE_ROLE, rank)
+        for _ in range(5):
+            bs.next()
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=ep.stream, capture_error_mode="thread_local"):
+            for _ in range(100):
+                bs.next()
+        graph.replay()
         torch.cuda.synchronize(dev)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(1, a.gathers // 100)
         g0.record(ep.stream)
-        for i in range(a.gathers):
-            random_batch_device(out, BatchRequest(32, 1000 + i), REC, slots)
+        for _ in range(reps):
+            graph.replay()
         g1.record(ep.stream)
         torch.cuda.synchronize(dev)
-        slots.check()
-        gather_ms = g0.elapsed_time(g1) / a.gathers
-    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases_all, walls))
+        bs.slots.check()
+        gather_ms = g0.elapsed_time(g1) / (100 * reps)
+        bulk = BatchSlots(a.bulk, REC, dev)
+        random_batch_device(out, BatchRequest(a.bulk, 1), REC, bulk)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(ep.stream)
+        for i in range(5):
+            random_batch_device(out, BatchRequest(a.bulk, 2 + i), REC, bulk)
+        b1.record(ep.stream)
+        torch.cuda.synchronize(dev)
+        bulk.check()
+        bulk_ms = b0.elapsed_time(b1) / 5
+        del bulk
+    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases_all, walls, bulk_ms))
     if rank == 0:
         wall = max(r[0] for r in rows)
         total = sum(r[2] for r in rows)
@@ -114,10 +146,18 @@ def main() -> None:
             "records_out": [r[2] for r in rows],
             "corrupt_records": sum(max(0, r[3]) for r in rows),
             "indices_bit_exact_vs_oracle": all(r[4] for r in rows) if not a.no_verify else None,
-            "gather_ms_per_batch32": max(r[5] for r in rows),
-            "gather_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
-            "gather_hbm_GBps": 2 * 32 * REC / (max(r[5] for r in rows) / 1e3) / 1e9,
+            "batch32_ms": max(r[5] for r in rows),
+            "batch32_is": "BatchStream.next() (picks + gather), 100 per CUDA graph, device time",
+            "batch32_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
+            "bulk_gather_records": a.bulk,
+            "bulk_gather_ms": max(r[8] for r in rows),
+            "bulk_gather_records_per_s_per_gpu": a.bulk / (max(r[8] for r in rows) / 1e3),
+            "bulk_gather_hbm_GBps": 2 * a.bulk * REC / (max(r[8] for r in rows) / 1e3) / 1e9,
         }
+        peak = _hbm_peak()
+        if peak:
+            line["bulk_gather_hbm_frac"] = line["bulk_gather_hbm_GBps"] / peak[0]
+            line["hbm_peak"] = {"GBps": peak[0], "source": peak[1]}
         if rows[0][6] and rows[0][6][-1]:
             line["phases_s_per_rank"] = [r[6] for r in rows]
         print(json.dumps(line), flush=True)
