@@ -21,6 +21,8 @@
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -63,6 +65,39 @@ __device__ void lemire_serial(uint64_t key, uint64_t count, uint32_t S, int32_t*
   }
 }
 
+// The same stream, block-parallel: numpy's Lemire-with-rejection makes draw k
+// the k-th Philox word w (w = 0, 1, ...) whose low product half is >= thr
+// (a first try with left < S re-tests left < thr, so "rejected" is exactly
+// left < thr). One CTA (blockDim % 32 == 0, every thread calls) compacts the
+// accepted words tile by tile with a ballot prefix. S >= 2.
+__device__ void block_lemire_compact(uint64_t key, uint32_t S, int64_t count, int64_t* out) {
+  __shared__ int warp_tot[32];
+  __shared__ long long s_have;
+  const uint32_t thr = static_cast<uint32_t>((0x100000000ULL - S) % S);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) s_have = 0;
+  __syncthreads();
+  for (uint64_t base = 0;; base += blockDim.x) {
+    const long long have = s_have;
+    if (have >= count) break;
+    const uint64_t m = static_cast<uint64_t>(philox_word32(key, base + tid)) * S;
+    const bool acc = static_cast<uint32_t>(m) >= thr;
+    const unsigned bal = __ballot_sync(0xffffffffu, acc);
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    int off = __popc(bal & ((1u << lane) - 1u));
+    for (int w = 0; w < wid; ++w) off += warp_tot[w];
+    if (acc && have + off < count) out[have + off] = static_cast<int64_t>(m >> 32);
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < nw; ++w) t += warp_tot[w];
+      s_have = have + t;
+    }
+    __syncthreads();
+  }
+}
+
 // random_batch picks (n_records may exceed 2^32 only in theory; the 32-bit
 // path covers n <= 2^32 exactly as numpy does).
 __global__ void picks_kernel(uint64_t key, uint32_t n, int64_t batch, int64_t* picks, int* bad) {
@@ -86,8 +121,8 @@ __global__ void __launch_bounds__(1024) picks_block_kernel(uint64_t key, uint32_
     else if (lemire_fast(key, static_cast<uint64_t>(i), n, &v)) picks[i] = v;
     else rejected = 1;
   }
-  if (__syncthreads_or(rejected) && i == 0)  // rare: redo the whole stream serially
-    lemire_serial(key, static_cast<uint64_t>(batch), n, nullptr, picks);
+  if (__syncthreads_or(rejected))  // rare: redo the stream with the rejections
+    block_lemire_compact(key, n, batch, picks);
 }
 // Graph-replayable variant: key from a device step counter, which it advances.
 __global__ void __launch_bounds__(1024) picks_step_kernel(uint64_t seed, uint64_t role,
@@ -106,13 +141,13 @@ __global__ void __launch_bounds__(1024) picks_step_kernel(uint64_t seed, uint64_
     else if (lemire_fast(key, static_cast<uint64_t>(i), n, &v)) picks[i] = v;
     else rejected = 1;
   }
-  if (__syncthreads_or(rejected) && i == 0)
-    lemire_serial(key, static_cast<uint64_t>(batch), n, nullptr, picks);
+  if (__syncthreads_or(rejected)) block_lemire_compact(key, n, batch, picks);
   if (i == 0) *step = st + 1;  // every thread read *step before the barrier above
 }
-__global__ void picks_serial_kernel(uint64_t key, uint32_t n, int64_t batch, int64_t* picks,
-                                    const int* bad) {
-  if (*bad) lemire_serial(key, static_cast<uint64_t>(batch), n, nullptr, picks);
+__global__ void __launch_bounds__(1024) picks_fix_kernel(uint64_t key, uint32_t n,
+                                                         int64_t batch, int64_t* picks,
+                                                         const int* bad) {
+  if (*bad) block_lemire_compact(key, n, batch, picks);
 }
 
 // ---- shuffle: destination draws of every source member ----------------------
@@ -436,6 +471,114 @@ __global__ void __launch_bounds__(512) gather_kernel(const uint8_t* blob, const 
   }
 }
 
+// Fixed-size gather on the TMA engines: each CTA (one warp, lane 0 issues)
+// owns a contiguous range of (record, 32 KiB chunk) units and streams them
+// through a ring of SMEM stages -- cp.async.bulk load (mbarrier) then
+// cp.async.bulk store -- so ~kGStages chunks per SM are in flight with no
+// register traffic; a record's metadata (picks -> off/len/label) is loaded
+// once per record. A record whose source is not 16-byte aligned is copied by
+// the warp directly. Opt-in (MD_GATHER_TMA=1): measured on B200 the LDG
+// kernel below is as fast for bulk gathers (6.3-6.5 vs 5.7-6.2 TB/s
+// read+write, tools/gather_probe.py) and faster for 32-record batches, where
+// its (record, chunk) units spread over more CTAs (5.9 vs 7.0 us).
+constexpr int kGStages = 6;
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// wait until at most `pending` bulk store groups may still read their SMEM
+__device__ __forceinline__ void bulk_wait_read(uint32_t pending) {
+  switch (pending) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+  }
+  static_assert(kGStages <= 6, "bulk_wait_read covers up to kGStages - 1 newer groups");
+}
+
+__global__ void __launch_bounds__(32, 1) gather_tma_kernel(
+    const uint8_t* blob, const uint64_t* off, const uint32_t* len, const uint32_t* label,
+    const int64_t* picks, int64_t batch, uint8_t* out, int64_t stride, uint32_t* out_label,
+    int32_t* bad, int chunks) {
+  extern __shared__ __align__(128) char gring[];
+  __shared__ __align__(8) uint64_t full[kGStages];
+  const int lane = threadIdx.x;
+  const int64_t units = batch * chunks;
+  const int64_t per = (units + gridDim.x - 1) / gridDim.x;
+  const int64_t u0 = static_cast<int64_t>(blockIdx.x) * per;
+  const int64_t u1 = min(units, u0 + per);
+  if (u0 >= u1) return;
+  if (lane == 0) {
+    for (int s = 0; s < kGStages; ++s) mbar_init(&full[s], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  uint8_t* pdst[kGStages];
+  uint32_t pbytes[kGStages];
+  int64_t cur_b = -1, next = u0;
+  const uint8_t* src = nullptr;
+  uint8_t* dst = nullptr;
+  uint32_t L = 0;
+  bool ok = false, aligned = false;
+  uint32_t issued = 0, stored = 0;  // ring sequence numbers
+  for (;;) {
+    while (next < u1 && issued - stored < kGStages) {
+      const int64_t b = next / chunks;
+      const int c = static_cast<int>(next % chunks);
+      ++next;
+      if (b != cur_b) {
+        cur_b = b;
+        const int64_t r = picks[b];
+        L = len[r];
+        src = blob + off[r];
+        dst = out + b * stride;
+        ok = static_cast<int64_t>(L) == stride;
+        aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+        if (lane == 0) {
+          if (!ok && bad) atomicExch(bad, 1);
+          if (ok && c == 0 && out_label) out_label[b] = label[r];
+        }
+      }
+      if (!ok) continue;
+      const uint64_t lo = static_cast<uint64_t>(c) * kGatherChunk;
+      if (lo >= L) continue;
+      const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(kGatherChunk), L - lo));
+      if (!aligned || (n & 15)) {  // rare: plain warp copy
+        for (uint32_t k = lane; k < n; k += 32) dst[lo + k] = src[lo + k];
+        continue;
+      }
+      const uint32_t st = issued % kGStages;
+      if (lane == 0) {
+        if (issued >= kGStages) bulk_wait_read(stored - 1 - (issued - kGStages));
+        mbar_expect_tx(&full[st], n);
+        tma_load_1d(gring + st * kGatherChunk, src + lo, n, &full[st]);
+      }
+      pdst[st] = dst + lo;
+      pbytes[st] = n;
+      ++issued;
+    }
+    if (stored == issued) {
+      if (next >= u1) break;
+      continue;
+    }
+    const uint32_t st = stored % kGStages;
+    if (lane == 0) {
+      while (!mbar_try_wait(&full[st], (stored / kGStages) & 1)) {
+      }
+      bulk_store(pdst[st], gring + st * kGatherChunk, pbytes[st]);
+    }
+    ++stored;
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 struct SegCopy {
   uint8_t* dst[MD_MAX_GROUP];
   const uint8_t* src[MD_MAX_GROUP];
@@ -599,7 +742,7 @@ int md_random_batch(uint64_t key, int64_t n_records, int64_t batch, int64_t* pic
                                                  picks, bad);
   MD_LAUNCH_CHECK();
   if (n_records > 1) {
-    picks_serial_kernel<<<1, 1, 0, s>>>(key, static_cast<uint32_t>(n_records), batch, picks, bad);
+    picks_fix_kernel<<<1, 1024, 0, s>>>(key, static_cast<uint32_t>(n_records), batch, picks, bad);
     MD_LAUNCH_CHECK();
   }
   MD_CUDA_TRY(cudaFreeAsync(bad, s));
@@ -632,6 +775,23 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
   }
   const int chunks =
       out_stride > 0 ? static_cast<int>((out_stride + kGatherChunk - 1) / kGatherChunk) : 1;
+  if (out_stride > 0 && (out_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+      getenv("MD_GATHER_TMA")) {
+    static std::atomic<uint32_t> attr_set[64];
+    int dev = 0;
+    MD_CUDA_TRY(cudaGetDevice(&dev));
+    constexpr int kSmem = kGStages * static_cast<int>(kGatherChunk);
+    if (dev < 0 || dev >= 64 || !attr_set[dev].exchange(1)) {
+      MD_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    }
+    const int64_t units = batch * chunks;
+    const int grid = static_cast<int>(std::min<int64_t>(units, sm_count(dev)));
+    gather_tma_kernel<<<grid, 32, kSmem, as_stream(stream)>>>(
+        blob, off, len, label, picks, batch, out, out_stride, out_label, err_flag, chunks);
+    MD_LAUNCH_CHECK();
+    return MD_OK;
+  }
   gather_kernel<<<record_grid(batch * chunks), 512, 0, as_stream(stream)>>>(
       blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
   MD_LAUNCH_CHECK();

@@ -182,3 +182,68 @@ def test_batch_stream_matches_keyed_batches_eager_and_graph():
     bs.slots.check()
     with pytest.raises(errors.InvalidConfig):
         BatchStream(store, 2000, 96, 7, SAMPLE_ROLE, 0)
+
+
+@pytest.mark.parametrize("lead", [0, 7])
+def test_fixed_size_gather_tma_path(monkeypatch, lead):
+    """The TMA gather (multi-chunk records, ragged last chunk, unaligned
+    sources after a 7-byte record, bad-length detection) byte-equal with the
+    host copy of the picked records and with the default LDG kernel."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(11 + lead)
+    L = 2 * 32768 + 1040  # three chunks, the last one ragged (multiple of 16)
+    recs = ([dimd.Record(b"x" * lead, 999)] if lead else []) + [
+        dimd.Record(rng.bytes(L), int(i)) for i in range(300)]
+    blob, idx = dimd.build_blob(recs)
+    st = shard_from_bytes(blob, parse_index(idx), 0, 1, 1, device=dev)
+    picks = torch.tensor([i + (1 if lead else 0) for i in rng.integers(0, 300, 700)],
+                         dtype=torch.int64, device=dev)
+    monkeypatch.setenv("MD_GATHER_TMA", "1")
+    slots = dimd.BatchSlots(700, L, dev)
+    slots.picks.copy_(picks)
+    dimd._gather_fixed(st, slots, 700, L)
+    torch.cuda.synchronize(dev)
+    slots.check()
+    host = np.stack([np.frombuffer(recs[int(p)].bytes, np.uint8) for p in picks.cpu()])
+    assert np.array_equal(slots.records.cpu().numpy(), host)
+    assert slots.labels.cpu().tolist() == [recs[int(p)].label for p in picks.cpu()]
+    monkeypatch.delenv("MD_GATHER_TMA")
+    ldg = dimd.BatchSlots(700, L, dev)
+    ldg.picks.copy_(picks)
+    dimd._gather_fixed(st, ldg, 700, L)
+    assert torch.equal(ldg.records, slots.records)
+    if lead:  # a picked record of the wrong size raises on check(), both kernels
+        for tma in (True, False):
+            if tma:
+                monkeypatch.setenv("MD_GATHER_TMA", "1")
+            bad = dimd.BatchSlots(700, L, dev)
+            bad.picks.copy_(picks)
+            bad.picks[3] = 0
+            dimd._gather_fixed(st, bad, 700, L)
+            with pytest.raises(errors.LengthMismatch):
+                bad.check()
+            monkeypatch.delenv("MD_GATHER_TMA", raising=False)
+
+
+@pytest.mark.parametrize("n", [2**31 + 1, 3 * 2**30, 160_000])
+def test_picks_rejection_heavy_streams(oracle, n):
+    """Ranges where numpy's Lemire rejects ~50 % / 25 % of words: every picks
+    kernel (one-CTA batch, graph step counter, multi-CTA + block fix-up)
+    reproduces Generator(Philox(key)).integers(0, n, batch) exactly."""
+    from paper_1711_00705_b200 import _lib
+    from paper_1711_00705_b200.dimd import _mix64
+
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    sp = _lib.stream_ptr(torch.cuda.current_stream(dev))
+    for key, batch in ((11, 700), (2**64 - 3, 1024), (5, 5000), (9, 70_000)):
+        picks = torch.empty(batch, dtype=torch.int64, device=dev)
+        _lib.check(lib.md_random_batch(key, n, batch, picks.data_ptr(), sp))
+        assert np.array_equal(picks.cpu().numpy(), oracle.random_batch_picks(key, n, batch))
+    step = torch.full((1,), 41, dtype=torch.int64, device=dev)
+    picks = torch.empty(1000, dtype=torch.int64, device=dev)
+    for st in (41, 42):
+        _lib.check(lib.md_random_batch_step(3, 4, 5, step.data_ptr(), n, 1000, picks.data_ptr(), sp))
+        want = oracle.random_batch_picks(_mix64(3, 4, 5, st), n, 1000)
+        assert np.array_equal(picks.cpu().numpy(), want)
+    assert int(step.item()) == 43
