@@ -268,38 +268,89 @@ __device__ __forceinline__ uint32_t mask_of(uint32_t s) {
 }
 
 // One warp: walk the word stream deciding which word each Fisher-Yates step
-// accepts (random_interval). state[0] = next step s (counts down), state[1] =
-// next word index; resumable when it runs out of pre-generated words.
-__global__ void fy_scan_kernel(const uint32_t* ws, int64_t n_words, int64_t word_base,
-                               uint32_t* J, int64_t* state) {
+// accepts (random_interval: v = word & mask(s), accepted iff v <= s).
+// state[0] = next step s (counts down), state[1] = next word index;
+// resumable when it runs out of pre-generated words.
+//
+// 64 words per step of the walk (two per lane). With the same mask for steps
+// s .. s-63 a word is accepted for sure if v <= s-63 and rejected for sure if
+// v > s; only words in between ("ambiguous") depend on how many earlier words
+// were accepted. So: consume every word up to and including the FIRST
+// ambiguous one -- the ones before it are decided, and it is decided exactly
+// by the count of accepted words before it. Words reach SMEM in 32 KiB tiles
+// by one TMA bulk copy each. (The serial one-word-at-a-time walk is left only
+// for s < 128 and windows where the mask changes.)
+constexpr int kFyTile = 8192;
+__global__ void __launch_bounds__(32) fy_scan_kernel(const uint32_t* ws, int64_t n_words,
+                                                     int64_t word_base, uint32_t* J,
+                                                     int64_t* state) {
+  __shared__ __align__(128) uint32_t tile[kFyTile];
+  __shared__ __align__(8) uint64_t bar;
+  constexpr uint32_t kAll = 0xffffffffu;
   const int lane = threadIdx.x;
+  const uint32_t lt = (1u << lane) - 1u;
   int64_t s = state[0];
   int64_t p = state[1];
+  int64_t t_lo = 0, t_hi = 0;  // tile = words [t_lo, t_hi) relative to word_base
+  uint32_t phase = 0;
+  if (lane == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
   uint32_t mask = mask_of(static_cast<uint32_t>(s));
   while (s > 0) {
-    int64_t idx = p - word_base + lane;
-    if (p - word_base + 32 > n_words) break;  // need more words
-    uint32_t my = ws[idx];
-    // Fast path (no serial dependence): with the same mask for steps s .. s-31,
-    // a lane's word is accepted for sure if v <= s - 31 (at most 31 earlier
-    // lanes can have been accepted) and rejected for sure if v > s. If no lane
-    // falls in between, accepted lane with rank r takes step s - r.
-    if (s >= 64 && mask_of(static_cast<uint32_t>(s - 31)) == mask) {
-      const uint32_t v = my & mask;
-      const bool acc = v <= static_cast<uint32_t>(s - 31);
-      const bool amb = !acc && v <= static_cast<uint32_t>(s);
-      if (!__any_sync(0xffffffffu, amb)) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, acc);
-        if (acc) J[s - __popc(bal & ((1u << lane) - 1u))] = v;
-        s -= __popc(bal);
-        mask = mask_of(static_cast<uint32_t>(s));
-        p += 32;
-        continue;
+    const int64_t rel = p - word_base;
+    if (rel + 64 + 3 > n_words) break;  // need more words (host resumes at p)
+    if (rel + 64 > t_hi) {
+      const int64_t lo = rel & ~int64_t(3);  // 16-byte aligned source
+      const int64_t cnt = min(static_cast<int64_t>(kFyTile), (n_words - lo) & ~int64_t(3));
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar, static_cast<uint32_t>(cnt * 4));
+        tma_load_1d(tile, ws + lo, static_cast<uint32_t>(cnt * 4), &bar);
       }
+      while (!mbar_try_wait(&bar, phase)) {
+      }
+      phase ^= 1;
+      t_lo = lo;
+      t_hi = lo + cnt;
     }
+    const int base = static_cast<int>(rel - t_lo);
+    if (s >= 128 && mask_of(static_cast<uint32_t>(s - 63)) == mask) {
+      const uint32_t su = static_cast<uint32_t>(s), sure = su - 63;
+      const uint32_t v0 = tile[base + lane] & mask, v1 = tile[base + 32 + lane] & mask;
+      const bool a0 = v0 <= sure, a1 = v1 <= sure;
+      const uint32_t A0 = __ballot_sync(kAll, a0), A1 = __ballot_sync(kAll, a1);
+      const uint32_t M0 = __ballot_sync(kAll, !a0 && v0 <= su);
+      const uint32_t M1 = __ballot_sync(kAll, !a1 && v1 <= su);
+      uint32_t acc0 = A0, acc1 = A1;
+      int used = 64;
+      if (M0) {
+        const int f = __ffs(M0) - 1;
+        acc0 = A0 & ((1u << f) - 1u);
+        acc1 = 0;
+        if (__shfl_sync(kAll, v0, f) <= su - __popc(acc0)) acc0 |= 1u << f;
+        used = f + 1;
+      } else if (M1) {
+        const int f = __ffs(M1) - 1;
+        acc1 = A1 & ((1u << f) - 1u);
+        if (__shfl_sync(kAll, v1, f) <= su - __popc(acc0) - __popc(acc1)) acc1 |= 1u << f;
+        used = 33 + f;
+      }
+      const int c0 = __popc(acc0);
+      if ((acc0 >> lane) & 1u) J[s - __popc(acc0 & lt)] = v0;
+      if ((acc1 >> lane) & 1u) J[s - c0 - __popc(acc1 & lt)] = v1;
+      s -= c0 + __popc(acc1);
+      mask = mask_of(static_cast<uint32_t>(s));
+      p += used;
+      continue;
+    }
+    const uint32_t my = tile[base + lane];
     int used = 32;
     for (int l = 0; l < 32; ++l) {
-      uint32_t v = __shfl_sync(0xffffffffu, my, l) & mask;
+      uint32_t v = __shfl_sync(kAll, my, l) & mask;
       if (v <= static_cast<uint32_t>(s)) {
         if (lane == 0) J[s] = v;
         --s;
@@ -939,8 +990,10 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
     while (true) {
       words_kernel<<<blocks_for(chunk + 64), 256, 0, s>>>(pkey, word_base, chunk + 64, ws);
       MD_LAUNCH_CHECK();
+      pt.mark("fy gen");
       fy_scan_kernel<<<1, 32, 0, s>>>(ws, chunk + 64, word_base, J, st);
       MD_LAUNCH_CHECK();
+      pt.mark("fy scan");
       MD_CUDA_TRY(cudaMemcpyAsync(st_h, st, sizeof(st_h), cudaMemcpyDeviceToHost, s));
       MD_CUDA_TRY(cudaStreamSynchronize(s));
       if (st_h[0] == 0) break;

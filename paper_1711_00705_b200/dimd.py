@@ -448,7 +448,10 @@ def group_record_counts(channel, members, n_records: int, m_segments: int) -> li
     destination draws -- and insist the group agrees on m_segments (dest keys
     depend on the segment index, dimd.py:308; the reference would deadlock
     on a disagreement, here it is an InvalidConfig on every member)."""
-    rows = channel.all_gather((int(n_records), int(m_segments)))
+    return _group_counts(channel.all_gather((int(n_records), int(m_segments))), members, m_segments)
+
+
+def _group_counts(rows, members, m_segments: int) -> list[int]:
     seen = [rows[m][1] for m in members]
     if any(x != m_segments for x in seen):
         raise InvalidConfig(f"group members disagree on m_segments: {seen}")
@@ -543,11 +546,16 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     # make every source's shard visible (sync: the blob must be complete)
     torch.cuda.current_stream(dev).synchronize()
     mark = _PhaseClock(dev)
-    n_rec = group_record_counts(ep, members, store.n_records, int(m_segments))
-    v_blob = ep.register_varlen(store.blob)
-    v_off = ep.register_varlen(store.off if store.n_records else torch.zeros(1, dtype=torch.int64, device=dev))
-    v_len = ep.register_varlen(store.length if store.n_records else torch.zeros(1, dtype=torch.int32, device=dev))
-    v_lab = ep.register_varlen(store.label if store.n_records else torch.zeros(1, dtype=torch.int32, device=dev))
+    # one host collective: the members' record counts (group_record_counts)
+    # and every source's shard arrays, mapped into this process
+    empty = store.n_records == 0
+    arrays = [store.blob,
+              torch.zeros(1, dtype=torch.int64, device=dev) if empty else store.off,
+              torch.zeros(1, dtype=torch.int32, device=dev) if empty else store.length,
+              torch.zeros(1, dtype=torch.int32, device=dev) if empty else store.label]
+    (v_blob, v_off, v_len, v_lab), rows = ep.register_varlen_many(
+        arrays, (int(store.n_records), int(m_segments)))
+    n_rec = _group_counts(rows, members, int(m_segments))
     mark("register")
     cap = max(1, sum(n_rec))
     fm = torch.empty(cap, dtype=torch.int32, device=dev)

@@ -136,6 +136,30 @@ class CudaEndpoint:
         rows = self.all_gather((nbytes, None, 0, ptr))
         return [p for (_, _, _, p) in rows]
 
+    def _exchange_pointers(self, items, extra=None):
+        """``_exchange_pointer`` for several (ptr, nbytes) at once -- ONE host
+        collective -- plus an optional per-rank payload gathered alongside.
+        Returns (per item: every rank's address, per rank: its payload)."""
+        if self.n_ranks == 1:
+            return [[p] for p, _ in items], [extra]
+        if self.multiprocess:
+            mine = []
+            for ptr, nbytes in items:
+                handle = C.create_string_buffer(_lib.IPC_BYTES)
+                off = C.c_uint64()
+                _lib.check(self.lib.md_mem_export(C.c_void_p(ptr), handle, C.byref(off)))
+                mine.append((nbytes, bytes(handle.raw), int(off.value), ptr))
+            rows = self.all_gather((mine, extra))
+            out = []
+            for i in range(len(items)):
+                out.append([row[i][3] if r == self.rank else _IMPORTS.get(row[i][1]) + row[i][2]
+                            for r, (row, _) in enumerate(rows)])
+            return out, [e for _, e in rows]
+        if self.mode == "p2p":
+            self._enable_peers()
+        rows = self.all_gather(([p for p, _ in items], extra))
+        return [[row[0][i] for row in rows] for i in range(len(items))], [row[1] for row in rows]
+
     _peers_enabled = False
 
     def _enable_peers(self) -> None:
@@ -176,6 +200,18 @@ class CudaEndpoint:
         nbytes = tensor.numel() * tensor.element_size()
         ptrs = self._exchange_pointer(tensor.data_ptr() if nbytes else 0, nbytes)
         return PeerView(ptrs, nbytes, tensor)
+
+    def register_varlen_many(self, tensors, extra=None):
+        """``register_varlen`` of several tensors in one host collective;
+        ``extra`` (any picklable) is all-gathered with the handles."""
+        items = []
+        for t in tensors:
+            if t.device != self.torch_device:
+                raise InvalidConfig(f"tensor on {t.device}, endpoint on {self.torch_device}")
+            nbytes = t.numel() * t.element_size()
+            items.append((t.data_ptr() if nbytes else 0, nbytes))
+        ptrs, extras = self._exchange_pointers(items, extra)
+        return [PeerView(p, nb, t) for p, (_, nb), t in zip(ptrs, items, tensors)], extras
 
     def alloc(self, n: int, dtype=torch.float32) -> tuple[torch.Tensor, PeerView]:
         """Collective allocation of a peer-registered tensor (zeroed)."""
