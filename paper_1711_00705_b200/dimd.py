@@ -462,35 +462,50 @@ LAST_SHUFFLE_PHASES: dict[str, float] = {}
 
 
 class _ShardArena:
-    """Reusable output blobs for successive shuffles of one endpoint.
+    """Reusable output allocations for successive shuffles of one endpoint.
 
-    Peers map a shard's blob through CUDA IPC (md_mem_import), and mapping a
-    24 GB allocation costs tens of ms; reusing the same few allocations makes
-    the mappings hits of the per-process import cache after the first epochs.
-    A slot is reused only when the ShardStore that owned it has been garbage
+    Peers map a shard's arrays through CUDA IPC (md_mem_import): mapping a
+    24 GB blob costs tens of ms, and even a fresh 1 MB index allocation costs
+    ~1-3 ms across the group (tools/register_probe.py). So each slot keeps a
+    blob allocation AND one index allocation (off | len | label) that are
+    reused epoch after epoch; the imports then hit the per-process cache. A
+    slot is reused only when the ShardStore that owned it has been garbage
     collected, so no live store is ever overwritten."""
 
     HEADROOM = 1.03
 
     def __init__(self):
-        self.slots: list[list] = []  # [tensor, weakref to owning store or None]
+        self.slots: list[list] = []  # [blob tensor, weakref to owner or None, index tensor]
 
-    def take(self, nbytes: int, device) -> tuple[torch.Tensor, list]:
-        import weakref  # noqa: F401
-
+    def take(self, n_records: int, device) -> tuple[tuple[torch.Tensor, ...], list]:
+        """A free slot and its (off int64, len int32, label int32) views."""
         free = [s for s in self.slots if s[1] is None or s[1]() is None]
-        for s in sorted(free, key=lambda s: s[0].numel()):
-            if s[0].numel() >= nbytes:
-                return s[0][: max(1, nbytes)], s
-        if free:  # grow the largest free slot
-            slot = max(free, key=lambda s: s[0].numel())
-            slot[0] = None
+        need = 16 * max(1, n_records)
+        fits = [s for s in free if s[2] is not None and s[2].numel() >= need]
+        if fits:
+            slot = min(fits, key=lambda s: s[2].numel())
+        elif free:
+            slot = max(free, key=lambda s: 0 if s[0] is None else s[0].numel())
         else:
-            slot = [None, None]
+            slot = [None, None, None]
             self.slots.append(slot)
-        slot[0] = torch.empty(max(1, int(nbytes * self.HEADROOM)), dtype=torch.uint8,
-                              device=device)
-        return slot[0][: max(1, nbytes)], slot
+        if slot[2] is None or slot[2].numel() < need:
+            slot[2] = None
+            slot[2] = torch.empty(int(need * self.HEADROOM) + 64, dtype=torch.uint8, device=device)
+        n = max(1, n_records)
+        raw = slot[2]
+        off = raw[: 8 * n].view(torch.int64)
+        ln = raw[8 * n: 12 * n].view(torch.int32)
+        lb = raw[12 * n: 16 * n].view(torch.int32)
+        slot[1] = None
+        return (off, ln, lb), slot
+
+    def blob(self, slot: list, nbytes: int, device) -> torch.Tensor:
+        if slot[0] is None or slot[0].numel() < nbytes:
+            slot[0] = None
+            slot[0] = torch.empty(max(1, int(nbytes * self.HEADROOM)), dtype=torch.uint8,
+                                  device=device)
+        return slot[0][: max(1, nbytes)]
 
     @staticmethod
     def bind(slot: list, store) -> None:
@@ -572,9 +587,8 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     )
     mark("plan")
     n_final = int(nf.value)
-    off = torch.empty(max(1, n_final), dtype=torch.int64, device=dev)
-    ln = torch.empty(max(1, n_final), dtype=torch.int32, device=dev)
-    lb = torch.empty(max(1, n_final), dtype=torch.int32, device=dev)
+    arena = _arena(ep)
+    (off, ln, lb), slot = arena.take(n_final, dev)
     total = C.c_uint64()
     _lib.check(
         lib.md_shuffle_index(
@@ -584,7 +598,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
         )
     )
     mark("index")
-    blob, slot = _arena(ep).take(int(total.value), dev)
+    blob = arena.blob(slot, int(total.value), dev)
     _lib.check(
         lib.md_shuffle_pull(
             S, _lib.ptr_array([v_blob.ptrs[m] for m in members]),

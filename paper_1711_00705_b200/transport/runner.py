@@ -124,6 +124,46 @@ def run_ranks(
     return RunResult(results, None, wall)
 
 
+def gpu_numa_node(device: int) -> int:
+    """NUMA node of a GPU's PCIe attachment (sysfs), -1 if unknown."""
+    try:
+        props = torch.cuda.get_device_properties(device)
+        bdf = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/numa_node") as f:
+            return int(f.read().strip())
+    except (OSError, ValueError, AttributeError):
+        return -1
+
+
+def _cpulist(text: str) -> set[int]:
+    cpus: set[int] = set()
+    for part in text.strip().split(","):
+        if "-" in part:
+            lo, hi = part.split("-")
+            cpus.update(range(int(lo), int(hi) + 1))
+        elif part:
+            cpus.add(int(part))
+    return cpus
+
+
+def bind_numa_local(device: int) -> int | None:
+    """Pin this process to the CPUs of its GPU's NUMA node, so pinned host
+    buffers it allocates afterwards (first touch) sit next to the GPU's PCIe
+    root. Returns the node, or None when unknown / not permitted."""
+    node = gpu_numa_node(device)
+    if node < 0:
+        return None
+    try:
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            cpus = _cpulist(f.read()) & os.sched_getaffinity(0)
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+    except OSError:
+        return None
+    return node
+
+
 def init_from_env(pull_timeout: float = DEFAULT_PULL_TIMEOUT) -> CudaEndpoint:
     """Endpoint for one process per GPU launched by torchrun (RANK, WORLD_SIZE,
     LOCAL_RANK, MASTER_ADDR/PORT in the environment). Peers are mapped with
