@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/mdb200.h"
@@ -43,6 +44,22 @@ extern std::atomic<uint64_t> g_launches;
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// The kernels that run back to back with the allreduce in a training step ask
+// for the max-shared carveout too, so the SM does not re-partition L1/SMEM
+// (a drain) between them and the 192 KB-SMEM allreduce. Once per device;
+// MD_DEFAULT_CARVEOUT=1 leaves the driver default (A/B switch).
+template <class K>
+inline void prefer_max_smem(K kernel, std::atomic<uint64_t>& done) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return;
+  const uint64_t bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  if (!getenv("MD_DEFAULT_CARVEOUT"))
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+  done.fetch_or(bit);
+}
 
 int sm_count(int device);
 

@@ -810,6 +810,8 @@ int md_random_batch_step(uint64_t seed, uint64_t role, uint64_t worker, int64_t*
     set_error("md_random_batch_step needs 1 <= batch <= 1024 and < 2^32 records");
     return MD_ERR_INVALID_CONFIG;
   }
+  static std::atomic<uint64_t> carve{0};
+  prefer_max_smem(picks_step_kernel, carve);
   picks_step_kernel<<<1, 1024, 0, as_stream(stream)>>>(
       seed, role, worker, step, static_cast<uint32_t>(n_records), batch, picks);
   MD_LAUNCH_CHECK();
@@ -843,6 +845,8 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
     MD_LAUNCH_CHECK();
     return MD_OK;
   }
+  static std::atomic<uint64_t> carve{0};
+  prefer_max_smem(gather_kernel, carve);
   gather_kernel<<<record_grid(batch * chunks), 512, 0, as_stream(stream)>>>(
       blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
   MD_LAUNCH_CHECK();

@@ -263,6 +263,8 @@ int md_fill_rank_input(float* buf, int64_t n, int32_t rank, int32_t n_ranks, voi
   if (n == 0) return MD_OK;
   // numpy: (rank + 1) * np.pi / n_ranks, evaluated left to right in float64
   double scale = (static_cast<double>(rank) + 1.0) * M_PI / static_cast<double>(n_ranks);
+  static std::atomic<uint64_t> carve{0};
+  prefer_max_smem(fill_kernel, carve);
   fill_kernel<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, as_stream(stream)>>>(buf, n, scale);
   MD_LAUNCH_CHECK();
   return MD_OK;

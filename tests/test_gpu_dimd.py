@@ -247,3 +247,30 @@ def test_picks_rejection_heavy_streams(oracle, n):
         want = oracle.random_batch_picks(_mix64(3, 4, 5, st), n, 1000)
         assert np.array_equal(picks.cpu().numpy(), want)
     assert int(step.item()) == 43
+
+
+def test_batch_stream_with_rejections(oracle):
+    """BatchStream (device step counter) over 40 steps of 1024 draws from
+    1,000,000 records -- ~21 % of the batches contain a Lemire rejection,
+    exercising the block-parallel compaction inside the step kernel."""
+    from paper_1711_00705_b200.dimd import BatchStream, _mix64
+    from paper_1711_00705_b200.sgd import SAMPLE_ROLE
+
+    dev = torch.device("cuda", 0)
+    n, L = 1_000_000, 16
+    st = dimd.synth_store(n, L, 0, 1, 3, 0, 1, 0, device=dev)
+    bs = BatchStream(st, 1024, L, 3, SAMPLE_ROLE, 7, start_step=100)
+    hit = 0
+    for step in range(100, 140):
+        recs, labels, picks = (t.clone() for t in bs.next())
+        want = oracle.random_batch_picks(_mix64(3, SAMPLE_ROLE, 7, step), n, 1024)
+        assert np.array_equal(picks.cpu().numpy(), want), step
+        gids = recs[:, :8].contiguous().view(torch.int64).flatten().cpu().numpy()
+        assert np.array_equal(gids, want)
+        assert torch.equal(labels, st.label[picks].to(torch.int32))
+        raw = oracle.gen(_mix64(3, SAMPLE_ROLE, 7, step)).bit_generator.random_raw(512)
+        w32 = np.stack([raw & 0xFFFFFFFF, raw >> np.uint64(32)], 1).ravel().astype(np.uint64)
+        hit += bool(np.any((w32 * np.uint64(n)) & np.uint64(0xFFFFFFFF) < (2**32 - n) % n))
+    assert hit >= 3  # the rejection path really ran
+    assert int(bs.step.item()) == 140
+    bs.slots.check()
