@@ -138,6 +138,7 @@ static int launch_sgd(float* w, const float* g, float* mom, int64_t n, float c, 
 // ---- fill pattern of bench.py:188-195 ----------------------------------------
 // The pattern has period 997: each CTA tabulates the 997 float32 values once
 // (same float64 expression, same rounding) and streams float4 stores.
+template <bool kStream>
 __global__ void __launch_bounds__(kThreads) fill_kernel(float* __restrict__ buf, int64_t n,
                                                         double scale) {
   __shared__ float tab[997];
@@ -149,8 +150,11 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(float* __restrict__ buf,
   if ((reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
     const int64_t nv = n / 4;
     float4* b4 = reinterpret_cast<float4*>(buf);
+    // (4 j) mod 997 advanced incrementally: no 64-bit modulo in the loop
+    uint32_t r0 = static_cast<uint32_t>((4 * first) % 997);
+    const uint32_t dr = static_cast<uint32_t>((4 * stride) % 997);
     for (int64_t j = first; j < nv; j += stride) {
-      uint32_t r = static_cast<uint32_t>((4 * j) % 997);
+      uint32_t r = r0;
       float4 x;
       x.x = tab[r];
       r = (r == 996) ? 0 : r + 1;
@@ -159,7 +163,10 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(float* __restrict__ buf,
       x.z = tab[r];
       r = (r == 996) ? 0 : r + 1;
       x.w = tab[r];
-      __stcs(b4 + j, x);
+      if (kStream) __stcs(b4 + j, x);
+      else b4[j] = x;
+      r0 += dr;
+      if (r0 >= 997) r0 -= 997;
     }
     for (int64_t i = nv * 4 + first; i < n; i += stride) buf[i] = tab[i % 997];
   } else {
@@ -263,9 +270,17 @@ int md_fill_rank_input(float* buf, int64_t n, int32_t rank, int32_t n_ranks, voi
   if (n == 0) return MD_OK;
   // numpy: (rank + 1) * np.pi / n_ranks, evaluated left to right in float64
   double scale = (static_cast<double>(rank) + 1.0) * M_PI / static_cast<double>(n_ranks);
-  static std::atomic<uint64_t> carve{0};
-  prefer_max_smem(fill_kernel, carve);
-  fill_kernel<<<grid_for((n + 3) / 4, kThreads), kThreads, 0, as_stream(stream)>>>(buf, n, scale);
+  // plain stores by default: the gradient stays in L2 for the allreduce that
+  // reads it next (MD_FILL_STREAM=1: evict-first stores, the A/B switch)
+  static std::atomic<uint64_t> carve0{0}, carve1{0};
+  const int grid = grid_for((n + 3) / 4, kThreads);
+  if (getenv("MD_FILL_STREAM")) {
+    prefer_max_smem(fill_kernel<true>, carve1);
+    fill_kernel<true><<<grid, kThreads, 0, as_stream(stream)>>>(buf, n, scale);
+  } else {
+    prefer_max_smem(fill_kernel<false>, carve0);
+    fill_kernel<false><<<grid, kThreads, 0, as_stream(stream)>>>(buf, n, scale);
+  }
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
