@@ -112,7 +112,8 @@ struct AllreduceArgs {
   int32_t has_update, vec_ok;
   float c, mu, wd_b;
   struct TraceEv* trace;  // nullable: per-CTA event log (MD_AR_TRACE=1)
-  int32_t flag_gpu_fence;  // publish with fence.acq_rel.gpu + relaxed sys stores
+  int32_t flag_gpu_fence;
+  int32_t reverse_local;   // local-only tasks walk their segments last-first  // publish with fence.acq_rel.gpu + relaxed sys stores
   ViewArgs v[MD_MAX_RANKS];
 };
 
@@ -890,7 +891,10 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
   // 16-byte loads: for pure HBM traffic that measured faster than the TMA ring
   // (81 % vs 72 % of HBM at N = 1, profiles/README.md)
   if (nrem == 0) {
-    for (int s = idx; s < nseg; s += m) {
+    for (int s0 = idx; s0 < nseg; s0 += m) {
+      // last segments first: a producer that just streamed the buffer (the
+      // step's gradient fill) left its END most recently in L2
+      const int s = a.reverse_local ? nseg - 1 - s0 : s0;
       SegGeom g = seg_geom(a, t, s, 0);
       if (kEpi != 0 && final_here && t.type == 0 && t.n_fold == 1 && a.n_workers == 0)
         lone_update<kEpi>(a, v, g.vlo, g.vhi, tid, blockDim.x);
@@ -1636,6 +1640,7 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   a.max_stage = max_stage;
   a.trace = nullptr;
   a.flag_gpu_fence = getenv("MD_AR_SYS_FENCE") == nullptr;  // see publish_flags
+  a.reverse_local = getenv("MD_AR_FORWARD") == nullptr;
   if (getenv("MD_AR_TRACE")) {  // diagnostics: one event log per device, per call
     const size_t bytes = sizeof(TraceEv) * 3 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
     if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
