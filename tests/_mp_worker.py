@@ -1,0 +1,89 @@
+"""torchrun worker for tests/test_gpu_multiproc.py: the multi-PROCESS path
+(one process per GPU, CUDA IPC handles over the gloo channel, plain kernel
+launch per rank) checked against the oracle. Prints one JSON line on rank 0.
+
+    torchrun --nproc-per-node N tests/_mp_worker.py
+"""
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle import oracle as O  # noqa: E402
+from paper_1711_00705_b200 import (  # noqa: E402
+    GradientBuffer,
+    SgdUpdate,
+    VarPayload,
+    allreduce,
+    alltoallv,
+    build_multicolor_trees,
+    dimd,
+)
+from paper_1711_00705_b200.transport import init_from_env  # noqa: E402
+
+
+def main() -> None:
+    ep = init_from_env()
+    N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
+    out: dict = {}
+    rng = np.random.default_rng(2017)
+    L, P = 100_003, 100_001
+    inputs = [rng.standard_normal(L).astype(np.float32) for _ in range(N)]
+    w0 = rng.standard_normal(P).astype(np.float32)
+    m0 = rng.standard_normal(P).astype(np.float32)
+    ks = [k for k in (1, 2, 4) if k <= N]
+    with torch.cuda.stream(ep.stream):
+        # 1. multicolor allreduce, bitwise vs the oracle fold, and the fused
+        #    momentum/weight-decay update vs the float32 restatement
+        for k in ks:
+            ts = build_multicolor_trees(N, k, 4)
+            want = O.fold_numpy(O.tables_from_trees(N, O.trees(N, k, 4)), inputs)
+            buf = GradientBuffer(torch.from_numpy(inputs[rank].copy()).to(dev))
+            w = torch.from_numpy(w0.copy()).to(dev)
+            m = torch.from_numpy(m0.copy()).to(dev)
+            upd = SgdUpdate(weights=w, c=0.0125, momentum=m, mu=0.9, wd_b=0.0032, update_len=P)
+            allreduce(ep, buf, "multicolor", tree_set=ts, segment_elems=1000, update=upd)
+            ep.synchronize()
+            w_want, m_want = O.sgd_np(w0, want[:P], m0.copy(), 0.0125, 0.9, 0.0032)
+            out[f"allreduce_k{k}"] = bool(np.array_equal(buf.data.cpu().numpy(), want))
+            out[f"update_k{k}"] = bool(np.array_equal(w.cpu().numpy(), w_want)
+                                       and np.array_equal(m.cpu().numpy(), m_want))
+        # 2. back-to-back calls on one registered buffer (device epochs)
+        g = GradientBuffer.alloc(4099, ep)
+        for _ in range(3):
+            g.data.fill_(float(rank + 1))
+            allreduce(ep, g, "multicolor", tree_set=build_multicolor_trees(N, ks[-1], 4))
+        ep.synchronize()
+        out["repeat"] = bool(torch.all(g.data == N * (N + 1) / 2).item())
+        # 3. DIMD shuffle: every slot's source index vs the oracle's plan, bytes
+        #    vs the generator (shard arrays mapped through IPC)
+        n = 3000
+        store = dimd.synth_store(n, 256, rank, N, 11, 0, N, rank, device=dev)
+        for epoch in range(2):
+            key = O.mix64(11, O.SHUF_ROLE, epoch)
+            counts = ep.all_gather(store.n_records)
+            new = dimd.shuffle_all(ep, store, m_segments=3, seed=key)
+            bad, gids = dimd.synth_verify(new, 11)
+            mem, rec = O.shuffle_plan_c(key, 0, N, rank, rank, 3, counts)
+            out[f"shuffle{epoch}_bytes"] = int(bad) == 0
+            out[f"shuffle{epoch}_count"] = new.n_records == len(mem)
+            store = new
+            if epoch == 0:
+                out["shuffle0_indices"] = bool(np.array_equal(gids.cpu().numpy(), mem + N * rec))
+        # 4. alltoallv (host payloads, device exchange)
+        mats = [[bytes([s, d]) * (s + d + 1) for d in range(N)] for s in range(N)]
+        got = alltoallv(ep, VarPayload.from_slices(mats[rank])).data
+        out["alltoallv"] = bytes(got) == b"".join(mats[s][rank] for s in range(N))
+    rows = ep.all_gather(out)
+    if rank == 0:
+        print(json.dumps({"n": N, "ok": all(all(r.values()) for r in rows), "rows": rows}))
+
+
+if __name__ == "__main__":
+    main()
