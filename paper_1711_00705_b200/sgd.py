@@ -278,3 +278,111 @@ def train_step(
     stats = StepStats(step=step, epoch=epoch, lr=lr, loss=float(tail[0]) / b,
                       correct=int(tail[1]), samples=b)
     return model, stats
+
+
+# -- the training loop around the step (sgd.py:430-570) ---------------------------------------
+
+
+@dataclass(frozen=True)
+class EpochMetrics:
+    epoch: int
+    loss: float
+    acc: float
+    time_s: float  # wall time (there is no simulated clock on real hardware)
+
+
+@dataclass(frozen=True)
+class TrainResult:
+    history: list[EpochMetrics]
+    steps: list[StepStats]
+    weights: np.ndarray
+    virtual_time: float | None
+    wall_time: float
+
+    @property
+    def final_acc(self) -> float:
+        return self.history[-1].acc
+
+
+def run_training(
+    cfg: TrainConfig,
+    corpus,
+    algo: str = "multicolor",
+    *,
+    grad_fn,
+    init_weights: np.ndarray,
+    backend: str = "cuda",
+    emulate: bool | None = None,
+    record_bytes: int | None = None,
+) -> TrainResult:
+    """Train for cfg.epochs over the corpus, one rank per node (sgd.py:470-542).
+
+    Each epoch optionally reshuffles the DIMD store (``shuffle_all`` keyed
+    ``_mix64(seed, "shuf", epoch)``), then runs max(1, len(corpus) //
+    effective_batch) steps of ``train_step``; metrics are identical on every
+    rank and rank 0's copy is returned. The store, the shuffle, the fused
+    fold + allreduce + update and the replica check run on the GPU; the
+    model's forward/backward is ``grad_fn`` (the reference's ToyModel is a
+    stand-in outside the hot path), and ``init_weights`` replaces
+    ``ToyModel.create``.
+    """
+    from paper_1711_00705_b200.dimd import build_blob, parse_index, shard_from_bytes, shuffle_all
+    from paper_1711_00705_b200.transport import run_ranks
+
+    if not corpus:
+        raise InvalidConfig("corpus must be non-empty")
+    blob, index = build_blob(corpus)
+    entries = parse_index(index)
+    steps_per_epoch = max(1, len(corpus) // cfg.effective_batch)
+    w0 = np.ascontiguousarray(init_weights, dtype=np.float32)
+
+    def program(ep):
+        import time
+
+        dev = ep.torch_device
+        with torch.cuda.device(dev), torch.cuda.stream(ep.stream):
+            store = shard_from_bytes(blob, entries, ep.rank, ep.n_ranks, cfg.group_size, device=dev)
+            model = DeviceModel.from_numpy(w0, dev, momentum=cfg.momentum != 0)
+            tree_set, ring = comm_plan(ep.n_ranks, algo)
+            buffers = StepBuffers(ep, model.n_params, cfg.workers_per_node)
+            t_start = time.perf_counter()
+            history: list[EpochMetrics] = []
+            rows: list[StepStats] = []
+            gstep = 0
+            for epoch in range(cfg.epochs):
+                if cfg.shuffle_every > 0 and epoch % cfg.shuffle_every == 0:
+                    store = shuffle_all(ep, store, seed=_mix64(cfg.seed, SHUFFLE_ROLE, epoch))
+                t0 = time.perf_counter()
+                loss_sum, correct = 0.0, 0
+                for _ in range(steps_per_epoch):
+                    model, st = train_step(
+                        ep, model, cfg, store, algo, step=gstep, epoch=gstep / steps_per_epoch,
+                        tree_set=tree_set, ring=ring, grad_fn=grad_fn, buffers=buffers,
+                        record_bytes=record_bytes,
+                    )
+                    st = StepStats(st.step, st.epoch, st.lr, st.loss, st.correct, st.samples,
+                                   elapsed_s=time.perf_counter() - t_start)
+                    rows.append(st)
+                    loss_sum += st.loss
+                    correct += st.correct
+                    gstep += 1
+                history.append(EpochMetrics(
+                    epoch=epoch, loss=loss_sum / steps_per_epoch,
+                    acc=correct / (steps_per_epoch * cfg.effective_batch),
+                    time_s=time.perf_counter() - t0,
+                ))
+            return model.weights.cpu().numpy(), history, rows
+
+    rr = run_ranks(cfg.n_nodes, backend, program, emulate=emulate)
+    weights, history, rows = rr.results[0]
+    return TrainResult(history=history, steps=rows, weights=weights,
+                       virtual_time=rr.virtual_time, wall_time=rr.wall_time)
+
+
+def metrics_csv(result: TrainResult) -> str:
+    """Per-step metrics stream: epoch,step,loss,acc,lr,elapsed_s (sgd.py:545-556)."""
+    lines = ["epoch,step,loss,acc,lr,elapsed_s"]
+    for st in result.steps:
+        lines.append(f"{int(st.epoch)},{st.step},{st.loss:.6g},{st.acc:.6g},"
+                     f"{st.lr:.6g},{st.elapsed_s:.6g}")
+    return "\n".join(lines) + "\n"

@@ -9,7 +9,7 @@ import torch
 
 from paper_1711_00705_b200 import DeviceModel, TrainConfig, build_multicolor_trees, run_ranks
 from paper_1711_00705_b200 import dimd, errors
-from paper_1711_00705_b200.sgd import StepBuffers, check_replicas, train_step
+from paper_1711_00705_b200.sgd import StepBuffers, check_replicas, lr_at, train_step
 
 pytestmark = pytest.mark.gpu
 
@@ -117,3 +117,61 @@ def test_train_step_validates_world_size():
                        grad_fn=lambda *a: None)
 
     run_ranks(2, "cuda", prog, emulate=True)
+
+
+def test_run_training_replays_on_host(oracle):
+    """run_training (sgd.py:470-556): 3 epochs x 4 steps on 2 ranks x 2 workers,
+    reshuffle every epoch. The gradient is each batch's label sum (integers:
+    exact under any fold order), so the final weights, every step's loss/acc
+    and the metrics CSV are replayed on the host from the oracle's shuffle
+    plan and random_batch picks."""
+    from paper_1711_00705_b200 import EpochMetrics, metrics_csv, run_training
+    from paper_1711_00705_b200.dimd import Record, default_segments
+    from paper_1711_00705_b200.sgd import SAMPLE_ROLE, SHUFFLE_ROLE, lr_schedule
+
+    recs = [Record(bytes([i]) * 16, i % 7) for i in range(64)]
+    cfg = TrainConfig(n_nodes=2, workers_per_node=2, per_worker_batch=4, epochs=3, base_lr=0.1,
+                      seed=5, group_size=1, shuffle_every=1)
+    p = 33
+    w0 = np.linspace(-1, 1, p).astype(np.float32)
+
+    def grad_fn(model, batches, bufs):
+        for (rec, lab, _), buf in zip(batches, bufs):
+            s = lab.to(torch.float32).sum()
+            buf[:p] = s
+            buf[p] = s
+            buf[p + 1] = (lab == 0).sum().to(torch.float32)
+
+    res = run_training(cfg, recs, grad_fn=grad_fn, init_weights=w0, record_bytes=16)
+
+    # host replay
+    sched = lr_schedule(cfg)
+    labels = np.array([r.label for r in recs])
+    order = [np.arange(64), np.arange(64)]  # each rank's shard (group_size 1: the whole corpus)
+    w = w0.copy()
+    t = 0
+    for epoch in range(3):
+        key = oracle.mix64(5, SHUFFLE_ROLE, epoch)
+        for r in range(2):
+            _, rec = oracle.shuffle_plan_c(key, r, 1, 0, r, default_segments(64 * 16), [64])
+            order[r] = order[r][rec]
+        for _ in range(4):
+            tot, zeros = 0, 0
+            for r in range(2):
+                for j in range(2):
+                    pk = oracle.random_batch_picks(oracle.mix64(5, SAMPLE_ROLE, 2 * r + j, t), 64, 4)
+                    lab = labels[order[r][pk]]
+                    tot += int(lab.sum())
+                    zeros += int((lab == 0).sum())
+            lr = lr_at(sched, t / 4)
+            st = res.steps[t]
+            assert st.step == t and st.lr == lr
+            assert st.loss == tot / 16 and st.correct == zeros
+            w = oracle.sub_scaled_np(w, np.full(p, tot, np.float32), lr / 16)
+            t += 1
+    assert np.array_equal(res.weights, w)
+    assert len(res.history) == 3 and isinstance(res.history[0], EpochMetrics)
+    assert res.history[1].loss == sum(s.loss for s in res.steps[4:8]) / 4
+    csv = metrics_csv(res).splitlines()
+    assert csv[0] == "epoch,step,loss,acc,lr,elapsed_s" and len(csv) == 13
+    assert csv[5].startswith(f"1,4,{res.steps[4].loss:.6g},{res.steps[4].acc:.6g},")

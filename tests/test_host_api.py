@@ -151,3 +151,17 @@ def test_gradient_buffer_host_constructors():
     c = GradientBuffer(np.arange(8, dtype=np.float32)[::2])
     assert c.data.flags.c_contiguous and c.data.tolist() == [0.0, 2.0, 4.0, 6.0]
     assert math.isfinite(float(c.data.sum()))
+
+
+def test_metrics_csv_format():
+    """metrics_csv (sgd.py:545-556): header + one row per step, %.6g fields."""
+    from paper_1711_00705_b200.sgd import EpochMetrics, StepStats, TrainResult, metrics_csv
+
+    steps = [StepStats(step=i, epoch=i / 3, lr=0.1 * (i + 1), loss=1.0 / (i + 1), correct=i,
+                       samples=4, elapsed_s=0.5 * i) for i in range(4)]
+    res = TrainResult(history=[EpochMetrics(0, 1.0, 0.5, 0.1)], steps=steps,
+                      weights=np.zeros(3, np.float32), virtual_time=None, wall_time=1.0)
+    assert metrics_csv(res) == (
+        "epoch,step,loss,acc,lr,elapsed_s\n"
+        "0,0,1,0,0.1,0\n0,1,0.5,0.25,0.2,0.5\n0,2,0.333333,0.5,0.3,1\n1,3,0.25,0.75,0.4,1.5\n")
+    assert res.final_acc == 0.5
