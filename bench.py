@@ -183,28 +183,64 @@ def run_ours(a) -> None:
         _lib.check(lib.md_fill_rank_input(grad.data.data_ptr(), P + 2, rank, N, sptr))
 
     ar_ev = []
+    # Input pipeline: the batch of step i+1 is drawn and gathered on a side
+    # stream into the other of two slot sets while the GPU works on earlier
+    # steps (a real loop's prefetch); step i's gradient producer waits for
+    # batch i, and a slot set is refilled only after its step consumed it.
+    # (Starting the prefetch later -- after step i-1's allreduce -- measured
+    # slower: 125 vs 106 us per step at N = 1.)
+    side = torch.cuda.Stream(device=dev)
+    bslots = [batches.slots, BatchSlots(BATCH, REC, dev)]
+    gathered = [torch.cuda.Event(), torch.cuda.Event()]
+    consumed = [torch.cuda.Event(), torch.cuda.Event()]
 
-    def step(timed=False):
-        batches.next()  # picks for step i = the stream's device counter, then the gather
-        fill()
-        if timed:  # external: the pair also works as event nodes inside a captured graph
-            e0 = torch.cuda.Event(enable_timing=True, external=True)
-            e1 = torch.cuda.Event(enable_timing=True, external=True)
-            e0.record(stream)
-        allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
+    def prefetch(i):
+        with torch.cuda.stream(side):
+            batches.next(bslots[i % 2])  # picks = the stream's device counter, then the gather
+            gathered[i % 2].record(side)
+
+    def run_steps(k, timed=False):
+        # `timed`: the allreduce measurement schedule -- the same steps with
+        # the input pipeline serialised (picks, gather, fill, allreduce on one
+        # stream, so the fused kernel runs alone) and event nodes around each
+        # allreduce (allreduce.ms, roofline). The headline graph has neither:
+        # event nodes between the kernels cost ~11 us per step at N = 1.
         if timed:
-            e1.record(stream)
-            ar_ev.append((e0, e1))
+            for _ in range(k):
+                batches.next(bslots[0])
+                fill()
+                e0 = torch.cuda.Event(enable_timing=True, external=True)
+                e1 = torch.cuda.Event(enable_timing=True, external=True)
+                e0.record(stream)
+                allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
+                e1.record(stream)
+                ar_ev.append((e0, e1))
+            return
+        side.wait_stream(stream)  # earlier steps consumed both slot sets
+        prefetch(0)
+        for i in range(k):
+            stream.wait_event(gathered[i % 2])
+            fill()  # the gradient producer consumes batch i
+            consumed[i % 2].record(stream)
+            if i + 1 < k:
+                if i >= 1:
+                    side.wait_event(consumed[(i + 1) % 2])
+                prefetch(i + 1)
+            allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
+
+    def check_slots():
+        for b in bslots:
+            b.check()
 
     with torch.cuda.stream(stream):
         # correctness before timing (reference bench.py:198-212 + 258-268):
         # closed-form f64 sum of the fill, rel err <= 1e-5
-        step()
+        run_steps(1)
         ep.synchronize()
-        batches.slots.check()
+        check_slots()
         key0 = dimd._mix64(SEED, SAMPLE_ROLE, rank, 0)
         want_picks = random_batch_picks(store, BatchRequest(BATCH, key0))
-        if not torch.equal(batches.slots.picks, want_picks):
+        if not torch.equal(bslots[0].picks, want_picks):
             raise SystemExit("device-keyed batch stream diverged from random_batch")
         idx = np.arange(0, P, 7919)
         got = grad.data[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
@@ -213,8 +249,7 @@ def run_ours(a) -> None:
         rel = float(np.max(np.abs(got - want) / np.abs(want)))
         if rel > 1e-5:
             raise SystemExit(f"allreduce result check failed: max rel err {rel:.3g}")
-        for _ in range(a.warmup):
-            step()
+        run_steps(a.warmup)
         ep.synchronize()
         graph = None
         if not a.no_graph:
@@ -224,11 +259,14 @@ def run_ours(a) -> None:
             l0 = lib.md_launch_count()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream, capture_error_mode="thread_local"):
-                for _ in range(a.steps):
-                    step(timed=True)
+                run_steps(a.steps)
             captured = lib.md_launch_count() - l0
+            graph_ar = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph_ar, stream=stream, capture_error_mode="thread_local"):
+                run_steps(a.steps, timed=True)
             ep.barrier()
             graph.replay()  # upload + one more warm pass of the same work
+            graph_ar.replay()
             ep.synchronize()
 
         # the sampler starts (and finishes initialising) before the barrier so
@@ -244,16 +282,20 @@ def run_ours(a) -> None:
         if graph is not None:
             graph.replay()
         else:
-            for _ in range(a.steps):
-                step(timed=True)
+            run_steps(a.steps, timed=True)
         t1.record(stream)
         torch.cuda.synchronize(dev)
         launches = captured if graph is not None else lib.md_launch_count() - l0
         ep.barrier()
         clk = clocks.stop() if clocks else None
         ep.take_error()
-        batches.slots.check()
+        check_slots()
         ms = t0.elapsed_time(t1)
+        if graph is not None:  # the serial schedule with event nodes around each allreduce
+            ep.barrier()
+            graph_ar.replay()
+            torch.cuda.synchronize(dev)
+            ep.take_error()
         ar_ms = sum(e0.elapsed_time(e1) for e0, e1 in ar_ev) / len(ar_ev)
         if os.environ.get("MD_BENCH_DEBUG"):
             print(json.dumps({"rank": rank, "ar_ms": [round(e0.elapsed_time(e1), 4)
@@ -332,7 +374,7 @@ def run_ours(a) -> None:
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
                 "algorithmic_bytes_per_launch": 2 * P * 4 * (N - 1) / N,
-                "kernel": "md::allreduce_kernel<4> (fused multicolor allreduce + SGD)"}
+                "kernel": "md::allreduce_channels_kernel<4> (fused multicolor allreduce + SGD)"}
     else:
         # lone rank: the fused kernel is the momentum/wd update: read g, r/w W and v
         algo_bytes = P * 20
@@ -340,7 +382,7 @@ def run_ours(a) -> None:
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                 "frac": achieved / peak_hbm, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes,
-                "kernel": "md::allreduce_kernel<4> (N=1: fused SGD momentum+wd epilogue)"}
+                "kernel": "md::allreduce_channels_kernel<4> (N=1: fused SGD momentum+wd epilogue)"}
     roof["traffic"] = _ncu_traffic(N)
     line = {
         "metric": METRIC,
@@ -365,6 +407,7 @@ def run_ours(a) -> None:
             "k_colors": ts.k if ts else 1, "arity": ts.arity if ts else None,
             "parallelism": f"dp{N}",
             "cuda_graph": not a.no_graph,
+            "input_pipeline": "batch i+1 drawn + gathered on a side stream (double-buffered slots) during step i",
             "l2": "inputs larger than L2 (W + momentum + gradient = 307 MB per GPU)",
         },
         "allreduce": {"ms": ar_ms, "bus_gbps": bus,

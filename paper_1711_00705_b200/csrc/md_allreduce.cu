@@ -645,6 +645,8 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __shared__ __align__(8) uint64_t tma_full[kStages];
   extern __shared__ __align__(128) char ring[];  // kRingBytes of TMA stages
   uint32_t tma_seq = 0;                          // chunks through the ring so far
+  pdl_wait();  // the step's producer (gradient fill / fold inputs) has completed
+  pdl_launch_dependents();
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
     for (int s = 0; s < kStages; ++s) mbar_init(&tma_full[s], 1);
@@ -1123,8 +1125,8 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __shared__ __align__(8) uint64_t ack[kDoneSlots];
   __shared__ int s_task, s_idx, s_m;
   extern __shared__ __align__(128) char ring[];
+  // prologue (SMEM only) overlaps the predecessor's drain under PDL
   if (tid == 0) {
-    s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
@@ -1140,6 +1142,9 @@ __global__ void __launch_bounds__(kArThreads, 1)
     s_idx = idx;
     s_m = m;
   }
+  pdl_wait();  // the step's producer (gradient fill / fold inputs) has completed
+  pdl_launch_dependents();
+  if (tid == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
   __syncthreads();
   const uint32_t epoch = s_epoch;
   int tn = kTraceHalf - 4;  // kernel-level events in the producer half's last slots
@@ -1662,8 +1667,12 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     MD_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(ctas * n_views), dim3(kArThreads), args,
                                             kRingBytes, as_stream(stream)));
   } else {
-    MD_CUDA_TRY(cudaLaunchKernel(kern, dim3(ctas), dim3(kArThreads), args, kRingBytes,
-                                 as_stream(stream)));
+    // programmatic dependent launch: the CTAs are scheduled while the
+    // predecessor drains and block in griddepcontrol.wait (md_common.cuh)
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    pdl_config(&cfg, at, dim3(ctas), dim3(kArThreads), kRingBytes, as_stream(stream));
+    MD_CUDA_TRY(cudaLaunchKernelExC(&cfg, kern, args));
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return MD_OK;

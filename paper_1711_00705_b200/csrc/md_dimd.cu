@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(1024) picks_step_kernel(uint64_t seed, uint64_
                                                           uint64_t worker, int64_t* step,
                                                           uint32_t n, int64_t batch,
                                                           int64_t* picks) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t st = *step;
   const uint64_t key =
       mix64_step(mix64_step(mix64_step(mix64_step(0, seed), role), worker),
@@ -503,6 +505,8 @@ __global__ void __launch_bounds__(512) gather_kernel(const uint8_t* blob, const 
                                                      int32_t* bad, int chunks) {
   // work unit = (record, chunk of kGatherChunk bytes): a 32-record batch of
   // 150 KB images spreads over ~150 CTAs instead of 32
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t units = batch * chunks;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t b = u / chunks;
@@ -812,8 +816,8 @@ int md_random_batch_step(uint64_t seed, uint64_t role, uint64_t worker, int64_t*
   }
   static std::atomic<uint64_t> carve{0};
   prefer_max_smem(picks_step_kernel, carve);
-  picks_step_kernel<<<1, 1024, 0, as_stream(stream)>>>(
-      seed, role, worker, step, static_cast<uint32_t>(n_records), batch, picks);
+  MD_CUDA_TRY(launch_pdl(picks_step_kernel, 1, 1024, 0, as_stream(stream), seed, role, worker,
+                         step, static_cast<uint32_t>(n_records), batch, picks));
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
@@ -847,8 +851,9 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
   }
   static std::atomic<uint64_t> carve{0};
   prefer_max_smem(gather_kernel, carve);
-  gather_kernel<<<record_grid(batch * chunks), 512, 0, as_stream(stream)>>>(
-      blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
+  MD_CUDA_TRY(launch_pdl(gather_kernel, record_grid(batch * chunks), 512, 0, as_stream(stream),
+                         blob, off, len, label, picks, batch, out, out_stride, out_off, out_label,
+                         err_flag, chunks));
   MD_LAUNCH_CHECK();
   return MD_OK;
 }

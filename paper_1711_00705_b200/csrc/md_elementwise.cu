@@ -28,6 +28,11 @@ void set_error(const char* fmt, ...) {
   t_err = buf;
 }
 
+bool pdl_enabled() {
+  static const bool on = getenv("MD_PDL") != nullptr;
+  return on;
+}
+
 int sm_count(int device) {
   static int cached[64] = {0};
   if (device < 0 || device >= 64) return 148;
@@ -145,6 +150,8 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(float* __restrict__ buf,
   for (int k = threadIdx.x; k < 997; k += blockDim.x)
     tab[k] = __double2float_rn(__dmul_rn(static_cast<double>(k) + 1.0, scale));
   __syncthreads();
+  pdl_wait();  // the table is private; the buffer may still be read by the last step
+  pdl_launch_dependents();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t first = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if ((reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
@@ -276,10 +283,10 @@ int md_fill_rank_input(float* buf, int64_t n, int32_t rank, int32_t n_ranks, voi
   const int grid = grid_for((n + 3) / 4, kThreads);
   if (getenv("MD_FILL_STREAM")) {
     prefer_max_smem(fill_kernel<true>, carve1);
-    fill_kernel<true><<<grid, kThreads, 0, as_stream(stream)>>>(buf, n, scale);
+    MD_CUDA_TRY(launch_pdl(fill_kernel<true>, grid, kThreads, 0, as_stream(stream), buf, n, scale));
   } else {
     prefer_max_smem(fill_kernel<false>, carve0);
-    fill_kernel<false><<<grid, kThreads, 0, as_stream(stream)>>>(buf, n, scale);
+    MD_CUDA_TRY(launch_pdl(fill_kernel<false>, grid, kThreads, 0, as_stream(stream), buf, n, scale));
   }
   MD_LAUNCH_CHECK();
   return MD_OK;

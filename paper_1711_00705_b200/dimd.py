@@ -357,20 +357,25 @@ class BatchStream:
         self.step = torch.full((1,), start_step, dtype=torch.int64, device=store.device)
         self.slots = BatchSlots(batch, record_bytes, store.device)
 
-    def next(self):
+    def next(self, slots: BatchSlots | None = None):
+        """Draw and gather the next step's batch into ``slots`` (default
+        ``self.slots``) on the current stream. A training loop that prefetches
+        (batch i+1 gathered on a side stream while step i computes) passes
+        alternating slot sets; the step counter still advances in stream order."""
         # Two launches (picks, gather). A fused one-kernel variant, where every
         # (record, chunk) CTA derives its own pick, measured slower on B200
         # (8.9 vs 6.0 us per 32-record batch): the per-CTA Philox + vote chain
         # is longer than the separate picks launch it saves.
         st = self.store
+        slots = self.slots if slots is None else slots
         _lib.check(
             _lib.load().md_random_batch_step(
                 self.seed, self.role, self.worker, self.step.data_ptr(), st.n_records, self.batch,
-                self.slots.picks.data_ptr(), _stream(st.device),
+                slots.picks.data_ptr(), _stream(st.device),
             )
         )
-        _gather_fixed(st, self.slots, self.batch, self.record_bytes)
-        return self.slots.records, self.slots.labels, self.slots.picks
+        _gather_fixed(st, slots, self.batch, self.record_bytes)
+        return slots.records, slots.labels, slots.picks
 
 
 def random_batch(store: ShardStore, req: BatchRequest) -> list[Record]:

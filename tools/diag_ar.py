@@ -50,7 +50,10 @@ def main() -> None:
     lags = [x for x in os.environ.get("DIAG_LAGS", "default").split(",")]
     with torch.cuda.stream(s):
         for name, kw in variants.items():
-            for mode, lag in [("free", g) for g in lags] + [("sync", "default")]:
+            modes = [("free", g) for g in lags] + [("sync", "default")]
+            if os.environ.get("DIAG_NOSYNC"):
+                modes = modes[:-1]
+            for mode, lag in modes:
                 if lag == "default":
                     os.environ.pop("MD_AR_LAG", None)
                 else:
@@ -80,7 +83,7 @@ def main() -> None:
 
         upd = variants["ar_sgd_mom_wd"]["update"]
         slots = BatchSlots(32, 150528, dev)
-        for shard in (2000, 160000):
+        for shard in (() if os.environ.get("DIAG_NOSTEP") else (2000, 160000)):
             store = dimd.synth_store(shard, 150528, rank, N, 1, 0, N, rank, device=dev)
             for clocks in (False, True):
                 sampler = None
