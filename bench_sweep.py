@@ -6,8 +6,12 @@
 
 Every configuration is checked before it is timed (the reference's rule,
 src/bench.py:258-268: the deterministic fill has a closed-form float64 sum,
-max rel err <= 1e-5). Times are CUDA-event medians of R runs, max over
-ranks; bus bandwidth = 2 * bytes * (N-1)/N / t (src/bench.py:116-119).
+max rel err <= 1e-5). Scenario "allreduce": device time per call -- G
+back-to-back calls captured in one CUDA graph (ours and NCCL alike), CUDA
+events around each of R replays, median / G, max over ranks. Scenario
+"allreduce_eager": host-launched calls (fill, event, call, event), which add
+each library's launch path (Python + ctypes / torch.distributed). Bus
+bandwidth = 2 * bytes * (N-1)/N / t (src/bench.py:116-119).
 Unconstructible (N, k, arity) triples are skipped like src/bench.py:224-232.
 Writes the reference's CSV schema to profiles/sweep_n{N}.csv (algorithm
 column carries k and arity) and prints one JSON line per row.
@@ -37,6 +41,8 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seg", type=int, default=0, help="segment_elems (0 = library default)")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--graph-calls", type=int, default=20, help="calls per captured graph")
+    ap.add_argument("--no-eager", action="store_true", help="graph-timed rows only")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
 
@@ -78,6 +84,8 @@ def main() -> None:
                                           _lib.stream_ptr(stream)))
 
     def timed(fn, n):
+        """Host-launched calls: fill, event, call, event (includes the
+        launch path of every call -- Python, ctypes / torch.distributed)."""
         ts = []
         for i in range(a.warmup + a.reps):
             fill(n)
@@ -91,6 +99,37 @@ def main() -> None:
         ep.take_error()
         med = statistics.median(e0.elapsed_time(e1) for e0, e1 in ts) / 1e3
         return max(ep.all_gather(med))
+
+    def timed_graph(fn, n):
+        """Device time per call: G back-to-back calls captured as ONE CUDA
+        graph, replayed R times; events around each replay, median / G, max
+        over ranks. (None if the call cannot be captured.)"""
+        G = a.graph_calls
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+                for _ in range(G):
+                    fn(n)
+        except Exception as e:  # noqa: BLE001
+            if rank == 0:
+                print(json.dumps({"graph_capture_failed": repr(e)[:200]}), flush=True)
+            ep.barrier()
+            return None
+        ep.barrier()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        ts = []
+        for _ in range(a.reps):
+            ep.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ts.append(e0.elapsed_time(e1) / G)
+        ep.take_error()
+        del g
+        return max(ep.all_gather(statistics.median(ts) / 1e3))
 
     def check(n, name):
         idx = np.arange(0, n, max(1, n // 4096))
@@ -114,8 +153,12 @@ def main() -> None:
                 torch.cuda.synchronize(dev)
                 ep.take_error()
                 check(n, f"multicolor k={k}")
-                t = timed(ours, n)
-                rows.append(("allreduce", f"multicolor_k{k}_a{arity}", N, size, t, "b200"))
+                t = timed_graph(ours, n)
+                if t is not None:
+                    rows.append(("allreduce", f"multicolor_k{k}_a{arity}", N, size, t, "b200"))
+                if not a.no_eager:
+                    t = timed(ours, n)
+                    rows.append(("allreduce_eager", f"multicolor_k{k}_a{arity}", N, size, t, "b200"))
             if nccl is not None:
                 def ref(n):
                     dist.all_reduce(buf.data[:n], group=nccl)
@@ -124,8 +167,12 @@ def main() -> None:
                 ref(n)
                 torch.cuda.synchronize(dev)
                 check(n, "nccl")
-                t = timed(ref, n)
-                rows.append(("allreduce", "nccl_allreduce", N, size, t, "nccl"))
+                t = timed_graph(ref, n)
+                if t is not None:
+                    rows.append(("allreduce", "nccl_allreduce", N, size, t, "nccl"))
+                if not a.no_eager:
+                    t = timed(ref, n)
+                    rows.append(("allreduce_eager", "nccl_allreduce", N, size, t, "nccl"))
 
     if rank == 0:
         out = Path(a.out) if a.out else ROOT / "profiles" / f"sweep_n{N}.csv"
@@ -134,7 +181,8 @@ def main() -> None:
         for sc, algo, n_r, size, t, be in rows:
             bus = 2 * size * (n_r - 1) / n_r / t / 1e9 if n_r > 1 else 0.0
             lines.append(f"{sc},{algo},{n_r},{size},{t!r},{bus!r},{be}")
-            print(json.dumps({"algorithm": algo, "n": n_r, "bytes": size, "us": t * 1e6,
+            print(json.dumps({"scenario": sc, "algorithm": algo, "n": n_r, "bytes": size,
+                              "us": t * 1e6,
                               "bus_GBps": bus, "backend": be}), flush=True)
         out.write_text("\n".join(lines) + "\n")
     ep.barrier()

@@ -25,6 +25,20 @@ from tests.test_oracle import GOLD_MC
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream"])
+def ar_path(request, monkeypatch):
+    """Every test runs on each kernel: the pipelined tree schedule
+    (allreduce_channels_kernel / the work-queue kernel), the one-shot pull
+    kernel, the LL push kernel and the tiled all-pull stream kernel -- the
+    last three evaluate the same fold programs locally, so the bits must not
+    change. (Sizes a path cannot take fall through to the tree schedule.)"""
+    big = str(1 << 40)
+    monkeypatch.setenv("MD_AR_ONESHOT_MAX", big if request.param == "oneshot" else "0")
+    monkeypatch.setenv("MD_AR_LL_MAX", big if request.param == "ll" else "0")
+    monkeypatch.setenv("MD_AR_STREAM", "1" if request.param == "stream" else "0")
+    return request.param
+
+
 def run(n, arrays, algo, emulate=True, **kw):
     def prog(ep):
         buf = GradientBuffer(torch.from_numpy(arrays[ep.rank].copy()).to(ep.torch_device))
@@ -82,6 +96,35 @@ def test_back_to_back_calls_reuse_flags_safely():
         return float(b.data[0])
 
     assert run_ranks(4, "cuda", prog, emulate=True).results == [24.0] * 4
+
+
+def test_oneshot_and_tree_calls_interleave(oracle, monkeypatch):
+    """Default thresholds: a 16 KB buffer takes the LL kernel, a 4.8 MB one
+    the tree schedule; alternating them on one communicator keeps the
+    epoch protocol (arrival / done flags) consistent and the bits exact."""
+    monkeypatch.delenv("MD_AR_ONESHOT_MAX", raising=False)
+    monkeypatch.delenv("MD_AR_LL_MAX", raising=False)
+    monkeypatch.delenv("MD_AR_STREAM", raising=False)
+    n = 4
+    ts = build_multicolor_trees(n, 4, 4)
+    tables = oracle.tables_from_trees(n, oracle.trees(n, 4, 4))
+    rng = np.random.default_rng(5)
+    small = [rng.standard_normal(4099).astype(np.float32) for _ in range(n)]
+    big = [rng.standard_normal(1_200_001).astype(np.float32) for _ in range(n)]
+    want_s, want_b = oracle.fold_c(tables, small), oracle.fold_c(tables, big)
+
+    def prog(ep):
+        dev = ep.torch_device
+        ok = []
+        for i in range(5):
+            src = small if i % 2 == 0 else big
+            buf = GradientBuffer(torch.from_numpy(src[ep.rank].copy()).to(dev))
+            allreduce_multicolor(ep, buf, ts)
+            ok.append(np.array_equal(buf.data.cpu().numpy(), want_s if i % 2 == 0 else want_b))
+        return ok
+
+    for r in run_ranks(n, "cuda", prog, emulate=True).results:
+        assert all(r)
 
 
 def test_host_numpy_buffers_are_a_drop_in(golden):
