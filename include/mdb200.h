@@ -120,6 +120,17 @@ int md_plan_destroy(md_plan_t* plan);
 /* One persistent kernel per call. `n_views` ranks are served by this call:
  * 1 for a real rank (one GPU per rank), n_ranks when every rank of the
  * world is emulated on one GPU (then comms[v] is rank v's communicator).
+ * The kernel is picked by size; all of them produce the same bits (the plan's
+ * fold order per color), which the GPU tests check for every path:
+ *   LL push      n*4 <= 1 MiB (N <= 4; 256 KiB above): every rank pushes
+ *                (value, epoch) words into its peers' control-block inbox and
+ *                folds locally -- one NVLink trip, no barrier (MD_AR_LL_MAX);
+ *   one-shot     N = 2 up to one SMEM pass of every rank's data (~14 MB):
+ *                pull every peer buffer, fold locally (MD_AR_ONESHOT_MAX);
+ *   tree         everything else (and worker folds / unaligned buffers): the
+ *                pipelined per-color reduce + broadcast over peer memory;
+ *   stream       opt-in (MD_AR_STREAM=1): tiled all-pull with per-tile
+ *                read-done flags.
  *
  *   bufs      [n_views * n_ranks]: for view v, rank r's gradient buffer as
  *             addressable from this process (peer-mapped); bufs[v*n+rank(v)]

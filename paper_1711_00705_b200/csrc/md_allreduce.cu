@@ -2157,12 +2157,13 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   if (has_update) epi = (a.v[0].mom ? 3 : 1) + (wd_b != 0.f ? 1 : 0);
 
   // LL (push) path for the smallest buffers: see allreduce_ll_kernel.
+  const int ll_avail = sm_count(dev) / n_views;
+  const int64_t ll_g = std::min<int64_t>(ll_avail, std::max<int64_t>(1, (n + 255) / 256));
+  const int64_t ll_e = ll_g > 0 ? (((n + ll_g - 1) / ll_g) + 3) & ~int64_t(3) : 0;
   if (N > 1 && n > 0 && n <= kLLElems && n_workers == 0 && a.vec_ok && plan->prog_dev &&
-      n * 4 <= ll_max_bytes(N)) {
-    const int avail = sm_count(dev) / n_views;
-    int64_t g = std::min<int64_t>(avail, std::max<int64_t>(1, (n + 255) / 256));
-    const int64_t E = (((n + g - 1) / g) + 3) & ~int64_t(3);
-    g = (n + E - 1) / E;
+      n * 4 <= ll_max_bytes(N) && ll_avail >= 1 && N * ll_e * 4 <= int64_t(kRingBytes)) {
+    const int64_t E = ll_e;
+    const int64_t g = (n + E - 1) / E;
     a.seg = E;
     a.ctas_per_view = static_cast<int32_t>(g);
     a.prog = plan->prog_dev;

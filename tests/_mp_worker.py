@@ -76,7 +76,31 @@ def main() -> None:
             store = new
             if epoch == 0:
                 out["shuffle0_indices"] = bool(np.array_equal(gids.cpu().numpy(), mem + N * rec))
-        # 4. alltoallv (host payloads, device exchange)
+        # 4. every allreduce kernel under CUDA-graph replay (device epochs,
+        #    LL inbox parity, read-done / arrival flags): 3 captured calls, each
+        #    on a refilled buffer, replayed twice; bitwise vs the oracle fold
+        ts = build_multicolor_trees(N, ks[-1], 4)
+        tabs = O.tables_from_trees(N, O.trees(N, ks[-1], 4))
+        for name, L2 in (("ll", 4099), ("oneshot", 400_003), ("tree", 6_000_001)):
+            src = [np.random.default_rng(r + L2).standard_normal(L2).astype(np.float32)
+                   for r in range(N)]
+            want2 = O.fold_numpy(tabs, src)
+            srcd = torch.from_numpy(src[rank]).to(dev)
+            gb = GradientBuffer.alloc(L2, ep)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=ep.stream, capture_error_mode="thread_local"):
+                for _ in range(3):
+                    gb.data.copy_(srcd)
+                    allreduce(ep, gb, "multicolor", tree_set=ts, check=False)
+            ok = True
+            for _ in range(2):
+                ep.barrier()
+                gr.replay()
+                ep.synchronize()
+                ep.take_error()
+                ok = ok and bool(np.array_equal(gb.data.cpu().numpy(), want2))
+            out[f"graph_{name}"] = ok
+        # 5. alltoallv (host payloads, device exchange)
         mats = [[bytes([s, d]) * (s + d + 1) for d in range(N)] for s in range(N)]
         got = alltoallv(ep, VarPayload.from_slices(mats[rank])).data
         out["alltoallv"] = bytes(got) == b"".join(mats[s][rank] for s in range(N))
