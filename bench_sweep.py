@@ -13,6 +13,8 @@ events around each of R replays, median / G, max over ranks. Scenario
 each library's launch path (Python + ctypes / torch.distributed). Bus
 bandwidth = 2 * bytes * (N-1)/N / t (src/bench.py:116-119).
 Unconstructible (N, k, arity) triples are skipped like src/bench.py:224-232.
+At N >= 4, for k < N and sizes above the LL range, rows "..._owner" time the
+owner-computes schedule (same fold order, same bits; md_plan_set_schedule).
 Writes the reference's CSV schema to profiles/sweep_n{N}.csv (algorithm
 column carries k and arity) and prints one JSON line per row.
 """
@@ -159,6 +161,21 @@ def main() -> None:
                 if not a.no_eager:
                     t = timed(ours, n)
                     rows.append(("allreduce_eager", f"multicolor_k{k}_a{arity}", N, size, t, "b200"))
+                if N >= 4 and k < N and size > (1 << 20):
+                    # owner-computes schedule: same fold order (same bits), balanced traffic
+                    def owner(n, ts=ts, view=view):
+                        allreduce(ep, view, "multicolor", tree_set=ts, segment_elems=seg,
+                                  check=False, schedule="owner")
+
+                    fill(n)
+                    owner(n)
+                    torch.cuda.synchronize(dev)
+                    ep.take_error()
+                    check(n, f"multicolor k={k} owner")
+                    t = timed_graph(owner, n)
+                    if t is not None:
+                        rows.append(("allreduce", f"multicolor_k{k}_a{arity}_owner", N, size, t,
+                                     "b200"))
             if nccl is not None:
                 def ref(n):
                     dist.all_reduce(buf.data[:n], group=nccl)

@@ -114,6 +114,15 @@ int md_plan_create(int32_t n_ranks, int32_t k, const int32_t* parent, const int3
                    const int32_t* child_idx, const int32_t* self_pos, int32_t device,
                    md_plan_t** out);
 int md_plan_destroy(md_plan_t* plan);
+/* Data movement of md_allreduce for this plan (never changes the bits):
+ * MD_SCHED_TREE (default) reduces and broadcasts each color along its own
+ * tree (collectives.py:225-296); MD_SCHED_OWNER cuts the buffer into n_ranks
+ * slices, rank j pulls slice j from every rank and evaluates each element's
+ * color fold in the tree's order, then every rank copies the final slices --
+ * 2 (n-1)/n of the buffer in per rank for any k. */
+#define MD_SCHED_TREE 0
+#define MD_SCHED_OWNER 1
+int md_plan_set_schedule(md_plan_t* plan, int32_t schedule);
 
 /* ---- allreduce: collectives.py:225-296 (multicolor), :302-359 (ring),
  *      :365-409 (reduce_then_broadcast); dispatcher :412-429 ----------------- */

@@ -19,6 +19,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libmdb200.so"
 MD_MAX_RANKS = 16
 MD_MAX_COLORS = 16
 MD_MAX_WORKERS = 8
+MD_SCHED_TREE = 0   # md_plan_set_schedule: per-color trees (the reference's schedule)
+MD_SCHED_OWNER = 1  # owner-computes slices, same bits
 MD_MAX_GROUP = 64
 IPC_BYTES = 64
 
@@ -56,6 +58,7 @@ SIGNATURES = {
          C.POINTER(_vp)],
     ),
     "md_plan_destroy": (C.c_int, [_vp]),
+    "md_plan_set_schedule": (C.c_int, [_vp, _i32]),
     "md_allreduce": (
         C.c_int,
         [_pp, _i32, _vp, _pp, _i64, _pp, _i32, _pp, _pp, _i64, _f32, _f32, _f32, _i64, _i32, _vp],

@@ -210,10 +210,18 @@ def run_fold(
     update: SgdUpdate | None = None,
     check: bool = True,
     ctas: int = 0,
+    schedule: str = "tree",
 ) -> GradientBuffer:
-    """One fused device collective: [worker fold] -> fold tree -> [SGD epilogue]."""
+    """One fused device collective: [worker fold] -> fold tree -> [SGD epilogue].
+
+    ``schedule``: "tree" moves the data along each color's tree (the
+    reference's schedule, collectives.py:225-296); "owner" cuts the buffer
+    into n slices that one rank each folds with the same per-color fold order,
+    then broadcasts -- the same bits, balanced traffic for any k."""
     if segment_elems < 1:
         raise InvalidConfig(f"segment_elems must be >= 1, got {segment_elems}")
+    if schedule not in ("tree", "owner"):
+        raise InvalidConfig(f"schedule must be 'tree' or 'owner', got {schedule!r}")
     if tables.n_ranks != ep.n_ranks:
         raise InvalidConfig(f"plan built for {tables.n_ranks} ranks, run has {ep.n_ranks}")
     dev, view, host = _device_tensor(ep, buf)
@@ -237,7 +245,7 @@ def run_fold(
             raise LengthMismatch("momentum shorter than the update range")
         upd = (update.weights.data_ptr(), mom.data_ptr() if mom is not None else None, ulen,
                float(update.c), float(update.mu), float(update.wd_b))
-    plan = ep.plan(tables)
+    plan = ep.plan(tables, schedule)
     arg = (ep.comm, view.ptrs, wk, upd)
     lib = _lib.load()
 

@@ -72,7 +72,8 @@ struct Ctrl {
 };
 
 struct Task {
-  int32_t type;  // 0 = UP (fold), 1 = DOWN (copy final from parent)
+  int32_t type;  // 0 = UP (fold), 1 = DOWN (copy final from parent),
+                 // 2 = OWNER (fold every rank's value with the element's color program)
   int32_t color;
   int32_t stage;
   int32_t n_fold;
@@ -140,7 +141,8 @@ struct AllreduceArgs {
   struct TraceEv* trace;  // nullable: per-CTA event log (MD_AR_TRACE=1)
   int32_t flag_gpu_fence;
   int32_t reverse_local;   // local-only tasks walk their segments last-first  // publish with fence.acq_rel.gpu + relaxed sys stores
-  const FoldProg* prog;    // one-shot kernel: every color's fold program
+  const FoldProg* prog;    // every color's fold program (one-shot / LL / stream / owner)
+  int32_t prog_k;          // colors of the fold programs (the plan's k; a.k counts owner slices)
   ViewArgs v[MD_MAX_RANKS];
 };
 
@@ -161,6 +163,9 @@ struct md_plan {
   md::RankPlan* dev;                   // n_ranks entries
   std::vector<md::RankPlan> host;
   md::FoldProg* prog_dev;              // the same trees as fold programs (one-shot kernel)
+  std::vector<md::RankPlan> owner_host;  // owner-computes schedule (MD_SCHED_OWNER)
+  md::RankPlan* owner_dev;
+  int32_t schedule;                    // MD_SCHED_TREE / MD_SCHED_OWNER
 };
 
 namespace md {
@@ -176,6 +181,41 @@ __host__ __device__ __forceinline__ int64_t nseg_of(int64_t start, int64_t len, 
   if (len <= 0) return 0;
   int64_t a = start & ~int64_t(3);
   return (start + len - a + seg - 1) / seg;
+}
+
+// ---- fold programs (ColorProg): a color's whole fold over rank slots ----------
+__device__ __forceinline__ int color_of(int64_t n, int k, int64_t i) {
+  const int64_t base = n / k, extra = n % k;
+  const int64_t big = (base + 1) * extra;  // the first `extra` chunks hold base + 1
+  if (i < big) return static_cast<int>(i / (base + 1));
+  return static_cast<int>(extra + (i - big) / base);
+}
+
+__device__ __forceinline__ float fold_prog(const ColorProg& p, float* slots, int64_t E,
+                                           int64_t e) {
+  int off = 0;
+  for (int j = 0; j < p.n_ops; ++j) {
+    const int cnt = p.op_cnt[j];
+    float acc = slots[p.items[off] * E + e];
+    for (int q = 1; q < cnt; ++q) acc = __fadd_rn(acc, slots[p.items[off + q] * E + e]);
+    slots[p.op_dst[j] * E + e] = acc;
+    off += cnt;
+  }
+  return slots[p.root * E + e];
+}
+
+__device__ __forceinline__ float4 fold_prog4(const ColorProg& p, float* slots, int64_t E,
+                                             int64_t e) {  // e: multiple of 4
+  int off = 0;
+  for (int j = 0; j < p.n_ops; ++j) {
+    const int cnt = p.op_cnt[j];
+    float4 acc = *reinterpret_cast<const float4*>(slots + p.items[off] * E + e);
+    for (int q = 1; q < cnt; ++q)
+      acc = add4(acc, *reinterpret_cast<const float4*>(slots + p.items[off + q] * E + e));
+    *reinterpret_cast<float4*>(slots + p.op_dst[j] * E + e) = acc;
+    off += cnt;
+  }
+  return *reinterpret_cast<const float4*>(slots + p.root * E + e);
 }
 
 // ---- device helpers -----------------------------------------------------------
@@ -484,6 +524,14 @@ __device__ __forceinline__ void item_data(const AllreduceArgs& a, const ViewArgs
   using E = Elem<kVec>;
   constexpr int W = E::W;
   constexpr int kCopyUnroll = 2 * kUnroll;  // a copy holds nothing else in registers
+  if (t.type == 2) {  // OWNER (edge elements only): every rank's value, color program
+    for (int64_t i = lo + tid; i < hi; i += nthr) {
+      float x[MD_MAX_RANKS];
+      for (int r = 0; r < a.n_ranks; ++r) x[r] = r == v.rank ? v.buf[i] : v.peer[r][i];
+      v.buf[i] = fold_prog(a.prog->c[color_of(a.n, a.prog_k, i)], x, 1, 0);
+    }
+    return;
+  }
   if (t.type == 1) {  // DOWN: copy the parent's final value
     const float* src = v.peer[t.parent];
     const int64_t cstep = static_cast<int64_t>(nthr) * W * kCopyUnroll;
@@ -909,7 +957,7 @@ __device__ __forceinline__ bool aborted(const ViewArgs& v) {
 template <int kEpi>
 __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Task& t, int idx,
                             int m, uint32_t epoch, char* ring, uint64_t* full, uint64_t* empty,
-                            uint64_t* done, uint64_t* ack) {
+                            uint64_t* done, uint64_t* ack, const FoldProg& prog) {
   const int tid = threadIdx.x;
   const bool final_here = (t.type == 1) || (t.parent < 0);
   const int nrem = t.type == 1 ? 1 : t.n_fold - 1;
@@ -945,7 +993,8 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
   // [remote sources in fold order][own value][W][momentum] (slots of C floats),
   // so the consumers never wait on a global load: they read SMEM and issue
   // fire-and-forget stores.
-  const bool tma_own = t.type == 0 && a.n_workers == 0;  // worker folds stay LDG
+  const bool tma_own = t.type != 1 && a.n_workers == 0;  // worker folds stay LDG
+  const bool owner = t.type == 2;  // stage slot r = rank r (own included), then W, momentum
   constexpr bool kMomT = kEpi >= 3;
   const bool tma_epi = kEpi != 0 && final_here;
   const int own_slot = nrem;
@@ -997,6 +1046,9 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         mbar_expect_tx(&full[st], bytes * (nrem + (tma_own ? 1 : 0)) + wbytes * (kMomT ? 2 : 1));
         if (t.type == 1) {
           tma_load_1d(stage, v.peer[t.parent] + clo, bytes, &full[st]);
+        } else if (owner) {
+          for (int r = 0; r < a.n_ranks; ++r)
+            tma_load_1d(stage + r * slot, (r == v.rank ? v.buf : v.peer[r]) + clo, bytes, &full[st]);
         } else {
           int q = 0;
           for (int j = 0; j < t.n_fold; ++j) {
@@ -1084,6 +1136,17 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         float4 acc;
         if (t.type == 1) {
           acc = stage[e];
+        } else if (owner) {  // the element's own color program over the rank slots
+          float* sf = reinterpret_cast<float*>(ring + st * kStageBytes);
+          const int c0 = color_of(a.n, a.prog_k, i);
+          if (color_of(a.n, a.prog_k, i + 3) == c0) {
+            acc = fold_prog4(prog.c[c0], sf, g.C, 4 * e);
+          } else {
+            acc.x = fold_prog(prog.c[c0], sf, g.C, 4 * e);
+            acc.y = fold_prog(prog.c[color_of(a.n, a.prog_k, i + 1)], sf, g.C, 4 * e + 1);
+            acc.z = fold_prog(prog.c[color_of(a.n, a.prog_k, i + 2)], sf, g.C, 4 * e + 2);
+            acc.w = fold_prog(prog.c[color_of(a.n, a.prog_k, i + 3)], sf, g.C, 4 * e + 3);
+          }
         } else {
           int q = 0;
           for (int jf = 0; jf < t.n_fold; ++jf) {
@@ -1152,7 +1215,11 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __shared__ __align__(8) uint64_t done[kDoneSlots];
   __shared__ __align__(8) uint64_t ack[kDoneSlots];
   __shared__ int s_task, s_idx, s_m;
+  __shared__ FoldProg prog;  // owner schedule only
   extern __shared__ __align__(128) char ring[];
+  if (a.prog)
+    for (int i = tid; i < static_cast<int>(sizeof(FoldProg) / 4); i += blockDim.x)
+      reinterpret_cast<uint32_t*>(&prog)[i] = reinterpret_cast<const uint32_t*>(a.prog)[i];
   // prologue (SMEM only) overlaps the predecessor's drain under PDL
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -1180,7 +1247,7 @@ __global__ void __launch_bounds__(kArThreads, 1)
   const bool ok = entry_barrier(a, v, local_cta, epoch);
   if (tid == 0) trace_ev(a, 0, tn, EV_ENTRY, s_task < 0 ? 0xffff : s_task);
   if (ok && s_task >= 0)
-    run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty, done, ack);
+    run_channel<kEpi>(a, v, rp.t[s_task], s_idx, s_m, epoch, ring, full, empty, done, ack, prog);
   __syncthreads();
   if (tid == 0) trace_ev(a, 0, tn, EV_EXIT, s_task < 0 ? 0xffff : s_task);
   exit_barrier(a, v, epoch);
@@ -1199,40 +1266,6 @@ __global__ void __launch_bounds__(kArThreads, 1)
 // 2 (N-1)/N x bytes: equal at N = 2, so there it serves every size that fits
 // one SMEM pass (N x E floats per CTA <= kRingBytes); at larger N only small
 // and mid-size buffers (host threshold, md_allreduce).
-__device__ __forceinline__ int color_of(int64_t n, int k, int64_t i) {
-  const int64_t base = n / k, extra = n % k;
-  const int64_t big = (base + 1) * extra;  // the first `extra` chunks hold base + 1
-  if (i < big) return static_cast<int>(i / (base + 1));
-  return static_cast<int>(extra + (i - big) / base);
-}
-
-__device__ __forceinline__ float fold_prog(const ColorProg& p, float* slots, int64_t E,
-                                           int64_t e) {
-  int off = 0;
-  for (int j = 0; j < p.n_ops; ++j) {
-    const int cnt = p.op_cnt[j];
-    float acc = slots[p.items[off] * E + e];
-    for (int q = 1; q < cnt; ++q) acc = __fadd_rn(acc, slots[p.items[off + q] * E + e]);
-    slots[p.op_dst[j] * E + e] = acc;
-    off += cnt;
-  }
-  return slots[p.root * E + e];
-}
-
-__device__ __forceinline__ float4 fold_prog4(const ColorProg& p, float* slots, int64_t E,
-                                             int64_t e) {  // e: multiple of 4
-  int off = 0;
-  for (int j = 0; j < p.n_ops; ++j) {
-    const int cnt = p.op_cnt[j];
-    float4 acc = *reinterpret_cast<const float4*>(slots + p.items[off] * E + e);
-    for (int q = 1; q < cnt; ++q)
-      acc = add4(acc, *reinterpret_cast<const float4*>(slots + p.items[off + q] * E + e));
-    *reinterpret_cast<float4*>(slots + p.op_dst[j] * E + e) = acc;
-    off += cnt;
-  }
-  return *reinterpret_cast<const float4*>(slots + p.root * E + e);
-}
-
 // all CTAs of this rank: count in; the last tells every peer "I have finished
 // reading your buffer" (done flag); then every CTA waits for every peer's.
 __device__ void read_done_barrier(const AllreduceArgs& a, const ViewArgs& v, uint32_t epoch,
@@ -1834,6 +1867,46 @@ static void build_fold_prog(const std::vector<RankPlan>& plans, int n, int k, Fo
   }
 }
 
+// Owner-computes schedule ("which data movement"): the
+// buffer is cut into n equal slices (chunk_of with n "colors"); rank j owns
+// slice j: it pulls every rank's slice j and evaluates each element's OWN
+// color fold program (task type 2), then every other rank copies the final
+// slice from j (DOWN). Same adds in the same order per element as the tree
+// schedule -- same bits -- but every rank ingests 2 (n-1)/n of the buffer for
+// any k, where the reference's trees cap k = 1 / 2 at N = 4 at 50 / 75 %.
+static void build_owner_plans(int n, std::vector<RankPlan>* out) {
+  out->assign(n, RankPlan{});
+  for (int j = 0; j < n; ++j) {
+    for (int r = 0; r < n; ++r) {
+      RankPlan& rp = (*out)[r];
+      Task t{};
+      t.color = j;
+      if (r == j) {
+        t.type = 2;
+        t.stage = 0;
+        t.parent = -1;
+        t.n_fold = n;
+        for (int q = 0; q < n; ++q) {
+          t.fold_src[q] = q;
+          t.fold_leaf[q] = 1;  // raw inputs: ready at the entry barrier
+        }
+        t.n_down = n - 1;
+        for (int q = 0, c = 0; q < n; ++q)
+          if (q != j) t.down[c++] = q;
+      } else {
+        t.type = 1;
+        t.stage = 1;
+        t.parent = j;
+        t.n_down = 0;
+      }
+      rp.t[rp.n_tasks++] = t;
+    }
+  }
+  for (auto& rp : *out)
+    std::stable_sort(rp.t, rp.t + rp.n_tasks,
+                     [](const Task& x, const Task& y) { return x.stage < y.stage; });
+}
+
 }  // namespace md
 
 using namespace md;
@@ -2006,13 +2079,20 @@ int md_plan_create(int32_t n_ranks, int32_t k, const int32_t* parent, const int3
   p->device = device;
   p->host = host;
   p->prog_dev = nullptr;
+  p->owner_dev = nullptr;
+  p->schedule = MD_SCHED_TREE;
   FoldProg prog;
   build_fold_prog(host, n_ranks, k, &prog);
+  build_owner_plans(n_ranks, &p->owner_host);
   cudaError_t e = cudaMalloc(&p->dev, sizeof(RankPlan) * n_ranks);
   if (e == cudaSuccess)
     e = cudaMemcpy(p->dev, host.data(), sizeof(RankPlan) * n_ranks, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&p->prog_dev, sizeof(FoldProg));
   if (e == cudaSuccess) e = cudaMemcpy(p->prog_dev, &prog, sizeof(FoldProg), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&p->owner_dev, sizeof(RankPlan) * n_ranks);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p->owner_dev, p->owner_host.data(), sizeof(RankPlan) * n_ranks,
+                   cudaMemcpyHostToDevice);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     set_error("md_plan_create: %s", cudaGetErrorString(e));
@@ -2023,6 +2103,15 @@ int md_plan_create(int32_t n_ranks, int32_t k, const int32_t* parent, const int3
   return MD_OK;
 }
 
+int md_plan_set_schedule(md_plan_t* p, int32_t schedule) {
+  if (!p || (schedule != MD_SCHED_TREE && schedule != MD_SCHED_OWNER)) {
+    set_error("bad plan or schedule %d", schedule);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  p->schedule = schedule;
+  return MD_OK;
+}
+
 int md_plan_destroy(md_plan_t* p) {
   if (!p) return MD_OK;
   int prev;
@@ -2030,6 +2119,7 @@ int md_plan_destroy(md_plan_t* p) {
   cudaSetDevice(p->device);
   cudaFree(p->dev);
   cudaFree(p->prog_dev);
+  cudaFree(p->owner_dev);
   cudaSetDevice(prev);
   delete p;
   return MD_OK;
@@ -2293,19 +2383,50 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     }
   }
 
+  // owner-computes schedule (md_plan_set_schedule, build_owner_plans): the
+  // same channelized kernel over the owner plan (n slices), each owner
+  // evaluating the plan's fold programs. Worker folds and unaligned buffers
+  // keep the tree schedule (same bits either way).
+  auto weighted_of = [&](const std::vector<RankPlan>& plans) {
+    int wmax = 0;
+    for (const RankPlan& rp : plans) {
+      int wt = 0;
+      for (int i = 0; i < rp.n_tasks; ++i) {
+        const Task& t = rp.t[i];
+        wt += t.type == 1 || t.n_fold > 1 || t.parent < 0 || n_workers > 0;
+      }
+      wmax = std::max(wmax, wt);
+    }
+    return wmax;
+  };
+  const int est_ctas = sm_count(dev) / n_views;
+  // (the owner plan needs the channelized kernel: one CTA per task at least)
+  const bool owner = plan->schedule == MD_SCHED_OWNER && N > 1 && n_workers == 0 && a.vec_ok &&
+                     !getenv("MD_AR_QUEUE") && plan->owner_dev && plan->prog_dev &&
+                     weighted_of(plan->owner_host) <= est_ctas;
+  const std::vector<RankPlan>& hp = owner ? plan->owner_host : plan->host;
+  if (owner) {
+    a.plan = plan->owner_dev;
+    a.k = N;
+    a.prog = plan->prog_dev;
+    a.prog_k = plan->k;
+    const int64_t ml = (n + N - 1) / N;
+    const int64_t sg = std::max<int64_t>(4, (seg_elems + 3) & ~int64_t(3));
+    const int64_t ms = ((ml + 3) / kMaxSegs + 4 + 3) & ~int64_t(3);
+    a.seg = std::max(sg, ms);
+    int64_t mx2 = 0;
+    for (int col = 0; col < N; ++col) {
+      int64_t st, ln;
+      chunk_of(n, N, col, &st, &ln);
+      mx2 = std::max(mx2, nseg_of(st, ln, a.seg));
+    }
+    a.max_nseg = static_cast<int32_t>(mx2);
+  }
+
   // 16-byte aligned buffers take the channelized TMA kernel; anything else
   // the work-queue kernel with its scalar path (MD_AR_QUEUE=1 forces it)
   // (and only when every task of every rank can own at least one CTA)
-  int weighted = 0;
-  for (const RankPlan& rp : plan->host) {
-    int wt = 0;
-    for (int i = 0; i < rp.n_tasks; ++i) {
-      const Task& t = rp.t[i];
-      wt += t.type == 1 || t.n_fold > 1 || t.parent < 0 || n_workers > 0;
-    }
-    weighted = std::max(weighted, wt);
-  }
-  const int est_ctas = sm_count(dev) / n_views;
+  const int weighted = weighted_of(hp);
   const bool chan = a.vec_ok && !getenv("MD_AR_QUEUE") && weighted <= est_ctas;
   switch (epi) {
     case 1: kern = chan ? (const void*)allreduce_channels_kernel<1> : (const void*)allreduce_kernel<1>; break;
@@ -2334,7 +2455,7 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   a.ctas_per_view = ctas;
   // lag: about one CTA wave of items per pipeline stage (override: MD_AR_LAG)
   int max_stage = 0, max_tasks = 1;
-  for (const RankPlan& rp : plan->host) {
+  for (const RankPlan& rp : hp) {
     max_tasks = std::max(max_tasks, rp.n_tasks);
     for (int i = 0; i < rp.n_tasks; ++i) max_stage = std::max(max_stage, rp.t[i].stage);
   }

@@ -220,11 +220,14 @@ class CudaEndpoint:
         return t, self.register(t)
 
     # -- plans --------------------------------------------------------------------------
-    def plan(self, tables) -> C.c_void_p:
-        fast = self._plans.get(id(tables))
+    def plan(self, tables, schedule: str = "tree") -> C.c_void_p:
+        """Device plan for fold tables (cached per tables object and schedule:
+        "tree" = the reference's per-color trees, "owner" = owner-computes
+        slices with the same fold order, md_plan_set_schedule)."""
+        fast = self._plans.get((id(tables), schedule))
         if fast is not None and fast[0] is tables:
             return fast[1]
-        key = tables.key()
+        key = (tables.key(), schedule)
         p = self._plans.get(key)
         if p is None:
             p = C.c_void_p()
@@ -243,8 +246,10 @@ class CudaEndpoint:
                         C.byref(p),
                     )
                 )
+                sched = _lib.MD_SCHED_OWNER if schedule == "owner" else _lib.MD_SCHED_TREE
+                _lib.check(self.lib.md_plan_set_schedule(p, sched))
             self._plans[key] = p
-        self._plans[id(tables)] = (tables, p)
+        self._plans[(id(tables), schedule)] = (tables, p)
         return p
 
     # -- errors / sync -------------------------------------------------------------------
