@@ -143,6 +143,7 @@ struct AllreduceArgs {
   int32_t reverse_local;   // local-only tasks walk their segments last-first  // publish with fence.acq_rel.gpu + relaxed sys stores
   const FoldProg* prog;    // every color's fold program (one-shot / LL / stream / owner)
   int32_t prog_k;          // colors of the fold programs (the plan's k; a.k counts owner slices)
+  int32_t warp_fence;      // channel kernel: consumer warps fence their own stores (MD_AR_WARP_FENCE)
   ViewArgs v[MD_MAX_RANKS];
 };
 
@@ -1099,7 +1100,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         s2 += m;
       }
       trace_ev(a, 2, cn, EV_DONE, pend[npend - 1]);
-      for (int i = 0; i < npend; ++i) publish_flags(a, v, t, pend[i], epoch, i == 0);
+      for (int i = 0; i < npend; ++i) publish_flags(a, v, t, pend[i], epoch, i == 0 && !a.warp_fence);
       trace_ev(a, 2, cn, EV_PUB, pend[npend - 1]);
       for (int i = 0; i < npend; ++i) {  // free the done slots for the consumers
         const uint32_t jj = j - npend + i;
@@ -1185,7 +1186,13 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
       if ((ct & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
     }
     // this warp is done with segment s: tell the notifier (the slot must have
-    // been acknowledged for the segment kDoneSlots earlier)
+    // been acknowledged for the segment kDoneSlots earlier). warp_fence
+    // (opt-in MD_AR_WARP_FENCE=1): the warp makes its own stores GPU-visible
+    // here and the notifier publishes without a fence; measured slower (N = 2
+    // fused 100 MB: 194 -> 213 us -- each warp then waits for its W/momentum
+    // stores), neutral at N = 4
+    if (a.warp_fence && !((t.type != 0 || t.parent < 0) && t.n_down == 0))
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if ((ct & 31) == 0) {
       if (jseg >= kDoneSlots) {
         uint32_t spins = 0;
@@ -2478,6 +2485,7 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   a.max_stage = max_stage;
   a.trace = nullptr;
   a.flag_gpu_fence = getenv("MD_AR_SYS_FENCE") == nullptr;  // see publish_flags
+  a.warp_fence = a.flag_gpu_fence && getenv("MD_AR_WARP_FENCE") != nullptr;
   a.reverse_local = getenv("MD_AR_FORWARD") == nullptr;
   if (getenv("MD_AR_TRACE")) {  // diagnostics: one event log per device, per call
     const size_t bytes = sizeof(TraceEv) * 3 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
