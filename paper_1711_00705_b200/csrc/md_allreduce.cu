@@ -1707,6 +1707,146 @@ __global__ void __launch_bounds__(kArThreads, 1)
   }
 }
 
+// ---- owner-push kernel (plain allreduce, large buffers) ---------------------------
+// Owner-computes with a PUSHED broadcast: rank j pulls slice j of every rank
+// through a TMA ring, folds each element with its color program (same bits),
+// and TMA-bulk-stores the final tile into its own buffer AND every peer's --
+// no DOWN tasks, no per-segment flags: a peer only needs every push into its
+// buffer to have landed before the call returns, which the exit barrier's
+// done flag certifies (each CTA waited for its bulk stores to complete).
+// Pulls and pushes split the 2 (N-1)/N bytes per rank between the two
+// protocols (measured ceilings: pull ~650, push ~688 GB/s bidirectional).
+// No fused epilogue (the receivers would need per-tile arrival signals).
+constexpr int kPushConsumerBase = 64;
+constexpr int kPushConsumerWarps = kArThreads / 32 - 2;
+
+__device__ __forceinline__ void bulk_store_nc(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kArThreads, 1)
+    allreduce_push_kernel(const __grid_constant__ AllreduceArgs a) {
+  const int view = blockIdx.x / a.ctas_per_view;
+  const int local_cta = blockIdx.x % a.ctas_per_view;
+  const int G = a.ctas_per_view;
+  const ViewArgs& v = a.v[view];
+  const int tid = threadIdx.x;
+  const int N = a.n_ranks, me = v.rank;
+  const int64_t TE = a.seg;
+  const int S = a.lag;
+  int64_t s0, sl;
+  chunk_of(a.n, N, me, &s0, &sl);  // my slice
+  const int64_t A = min(s0 + sl, (s0 + 3) & ~int64_t(3));
+  const int64_t B = max(A, (s0 + sl) & ~int64_t(3));
+  const int64_t T = (B - A + TE - 1) / TE;
+  const size_t slot_f = static_cast<size_t>(TE);
+  const size_t stage_f = slot_f * (N + 1);  // [N rank slots][result]
+  __shared__ uint32_t s_epoch;
+  __shared__ __align__(8) uint64_t full[8], empty[8], folded[8];
+  __shared__ FoldProg prog;
+  extern __shared__ __align__(128) char ring[];
+  float* ringf = reinterpret_cast<float*>(ring);
+  for (int i = tid; i < static_cast<int>(sizeof(FoldProg) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&prog)[i] = reinterpret_cast<const uint32_t*>(a.prog)[i];
+  if (tid == 0) {
+    s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+      mbar_init(&folded[st], kPushConsumerWarps);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  const bool ok = entry_barrier(a, v, local_cta, epoch);
+  if (ok) [&]() {
+    if (tid < 32) {  // ---------------- producer (+ the slice's unaligned edges) ----------------
+      if (tid != 0) return;
+      if (local_cta == 0) {
+        for (int64_t i = s0; i < s0 + sl; ++i) {
+          if (i >= A && i < B) {
+            i = B - 1;
+            continue;
+          }
+          float x[MD_MAX_RANKS];
+          for (int r = 0; r < N; ++r) x[r] = r == me ? v.buf[i] : v.peer[r][i];
+          const float g = fold_prog(prog.c[color_of(a.n, a.k, i)], x, 1, 0);
+          for (int r = 0; r < N; ++r) (r == me ? v.buf : const_cast<float*>(v.peer[r]))[i] = g;
+        }
+        __threadfence_system();  // edge pushes are generic stores: visible before our done flag
+      }
+      fence_proxy_async_global();
+      uint32_t seq = 0;
+      for (int64_t t = local_cta; t < T; t += G, ++seq) {
+        const uint32_t st = seq % S;
+        if (seq >= static_cast<uint32_t>(S)) {
+          uint32_t spins = 0;
+          while (!mbar_try_wait(&empty[st], ((seq / S) - 1) & 1))
+            if ((++spins & 1023) == 0 && aborted(v)) return;
+        }
+        const int64_t lo = A + t * TE, hi = min(B, lo + TE);
+        const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
+        float* stage = ringf + st * stage_f;
+        mbar_expect_tx(&full[st], bytes * N);
+        for (int r = 0; r < N; ++r)
+          tma_load_1d(stage + r * slot_f, (r == me ? v.buf : v.peer[r]) + lo, bytes, &full[st]);
+      }
+    } else if (tid < kPushConsumerBase) {  // ---------------- storer ----------------
+      if (tid != 32) return;
+      uint32_t seq = 0;
+      for (int64_t t = local_cta; t < T; t += G, ++seq) {
+        const uint32_t st = seq % S;
+        uint32_t spins = 0;
+        while (!mbar_try_wait(&folded[st], (seq / S) & 1))
+          if ((++spins & 1023) == 0 && aborted(v)) return;
+        const int64_t lo = A + t * TE, hi = min(B, lo + TE);
+        const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
+        const float* res = ringf + st * stage_f + N * slot_f;
+        for (int q = 0; q < N; ++q) {  // own buffer last: peers' pushes first on the wire
+          const int r = (me + 1 + q) % N;
+          bulk_store_nc((r == me ? v.buf : const_cast<float*>(v.peer[r])) + lo, res, bytes);
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (seq >= 1) {  // the previous tile's stores have read their SMEM: free its stage
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[(seq - 1) % S]))
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every push has landed
+    } else {  // ---------------- fold ----------------
+      const int ct = tid - kPushConsumerBase, nct = kPushConsumerWarps * 32;
+      uint32_t seq = 0;
+      for (int64_t t = local_cta; t < T; t += G, ++seq) {
+        const uint32_t st = seq % S;
+        uint32_t spins = 0;
+        while (!mbar_try_wait(&full[st], (seq / S) & 1))
+          if ((++spins & 1023) == 0 && aborted(v)) return;
+        float* stage = ringf + st * stage_f;
+        float* res = stage + N * slot_f;
+        const int64_t lo = A + t * TE, len = min(B, lo + TE) - lo;
+        for (int64_t e = 4 * ct; e < len; e += 4 * nct) {
+          const int c0 = color_of(a.n, a.k, lo + e);
+          if (color_of(a.n, a.k, lo + e + 3) == c0) {
+            *reinterpret_cast<float4*>(res + e) = fold_prog4(prog.c[c0], stage, slot_f, e);
+          } else {
+            for (int q = 0; q < 4; ++q)
+              res[e + q] = fold_prog(prog.c[color_of(a.n, a.k, lo + e + q)], stage, slot_f, e + q);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // SMEM -> bulk-store reads
+        __syncwarp();
+        if ((ct & 31) == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&folded[st])) : "memory");
+      }
+    }
+  }();
+  exit_barrier(a, v, epoch);
+}
+
 struct TraceBuf {
   void* ptr = nullptr;
   size_t bytes = 0, used = 0;
@@ -2132,6 +2272,15 @@ int md_plan_destroy(md_plan_t* p) {
   return MD_OK;
 }
 
+// Smallest plain buffer (bytes) the owner-push kernel takes by default.
+// Measured against the tree (graph-timed sweep, profiles/README.md): N = 2
+// faster from 64 MiB (117 vs 127 us; 1 GiB 662 vs 645 GB/s bus) but slower at
+// 16 MiB; N = 4 faster from 4 MiB (31.6 vs 34.6 us) to 1 GiB (622 vs 601),
+// within 2 % at 256 MiB.
+static int64_t push_min_bytes(int N) {
+  return N == 2 ? (int64_t(32) << 20) : (int64_t(2) << 20);
+}
+
 // Pipeline segment cap for a color chunk of `chunk` elements: about two
 // segments per SM, never below 4096 elements (the per-segment flag cost).
 // segment_elems is an upper bound only -- the bits never depend on it
@@ -2400,6 +2549,48 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return MD_OK;
       }
+    }
+  }
+
+  // owner-push kernel: plain allreduce (no fused epilogue, no worker fold)
+  // from push_min_bytes(N) up; MD_AR_PUSH=0 disables it, =1 forces it
+  const char* pe = getenv("MD_AR_PUSH");
+  const bool push_want = pe ? atoi(pe) != 0 : n * 4 >= push_min_bytes(N);
+  if (push_want && epi == 0 && N > 1 && n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
+    int64_t TE = 4096;
+    if (const char* te = getenv("MD_AR_TILE")) TE = std::max<int64_t>(4, atoll(te) & ~int64_t(3));
+    const int64_t stage_bytes = static_cast<int64_t>(N + 1) * TE * 4;
+    const int S = static_cast<int>(std::min<int64_t>(8, kRingBytes / stage_bytes));
+    const int avail = sm_count(dev) / n_views;
+    if (S >= 2 && avail >= 1) {
+      int64_t mx_t = 1;
+      for (int j = 0; j < N; ++j) {
+        int64_t st0, ln;
+        chunk_of(n, N, j, &st0, &ln);
+        mx_t = std::max(mx_t, (ln + TE - 1) / TE);
+      }
+      const int g = static_cast<int>(std::min<int64_t>(avail, mx_t));
+      a.seg = TE;
+      a.lag = S;
+      a.ctas_per_view = g;
+      a.prog = plan->prog_dev;
+      const void* pk = (const void*)allreduce_push_kernel;
+      static std::atomic<uint32_t> pk_set[64];
+      if (dev < 0 || dev >= 64 || !pk_set[dev].exchange(1)) {
+        MD_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kRingBytes)));
+      }
+      const size_t smem = static_cast<size_t>(S) * stage_bytes;
+      void* args[] = {&a};
+      if (n_views > 1 || getenv("MD_AR_COOP")) {
+        MD_CUDA_TRY(cudaLaunchCooperativeKernel(pk, dim3(static_cast<unsigned>(g) * n_views),
+                                                dim3(kArThreads), args, smem, as_stream(stream)));
+      } else {
+        MD_CUDA_TRY(cudaLaunchKernel(pk, dim3(static_cast<unsigned>(g)), dim3(kArThreads), args,
+                                     smem, as_stream(stream)));
+      }
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return MD_OK;
     }
   }
 

@@ -25,17 +25,20 @@ from tests.test_oracle import GOLD_MC
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream"])
+@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream", "push"])
 def ar_path(request, monkeypatch):
     """Every test runs on each kernel: the pipelined tree schedule
     (allreduce_channels_kernel / the work-queue kernel), the one-shot pull
-    kernel, the LL push kernel and the tiled all-pull stream kernel -- the
-    last three evaluate the same fold programs locally, so the bits must not
-    change. (Sizes a path cannot take fall through to the tree schedule.)"""
+    kernel, the LL push kernel, the tiled all-pull stream kernel and the
+    owner-push kernel -- the last four evaluate the same fold programs
+    locally, so the bits must not change. (Calls a path cannot take -- fused
+    epilogues for push, sizes beyond a path's range -- fall through to the
+    tree schedule.)"""
     big = str(1 << 40)
     monkeypatch.setenv("MD_AR_ONESHOT_MAX", big if request.param == "oneshot" else "0")
     monkeypatch.setenv("MD_AR_LL_MAX", big if request.param == "ll" else "0")
     monkeypatch.setenv("MD_AR_STREAM", "1" if request.param == "stream" else "0")
+    monkeypatch.setenv("MD_AR_PUSH", "1" if request.param == "push" else "0")
     return request.param
 
 
@@ -105,6 +108,7 @@ def test_oneshot_and_tree_calls_interleave(oracle, monkeypatch):
     monkeypatch.delenv("MD_AR_ONESHOT_MAX", raising=False)
     monkeypatch.delenv("MD_AR_LL_MAX", raising=False)
     monkeypatch.delenv("MD_AR_STREAM", raising=False)
+    monkeypatch.delenv("MD_AR_PUSH", raising=False)
     n = 4
     ts = build_multicolor_trees(n, 4, 4)
     tables = oracle.tables_from_trees(n, oracle.trees(n, 4, 4))

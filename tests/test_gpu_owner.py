@@ -31,6 +31,7 @@ def _owner_plan_only(monkeypatch):
     monkeypatch.setenv("MD_AR_LL_MAX", "0")
     monkeypatch.setenv("MD_AR_ONESHOT_MAX", "0")
     monkeypatch.setenv("MD_AR_STREAM", "0")
+    monkeypatch.setenv("MD_AR_PUSH", "0")
 
 
 def run(n, arrays, algo, emulate=True, **kw):
