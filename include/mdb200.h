@@ -136,8 +136,13 @@ int md_plan_set_schedule(md_plan_t* plan, int32_t schedule);
  *                folds locally -- one NVLink trip, no barrier (MD_AR_LL_MAX);
  *   one-shot     N = 2 up to one SMEM pass of every rank's data (~14 MB):
  *                pull every peer buffer, fold locally (MD_AR_ONESHOT_MAX);
- *   tree         everything else (and worker folds / unaligned buffers): the
- *                pipelined per-color reduce + broadcast over peer memory;
+ *   owner-push   plain buffers (no fused update / worker fold) from 32 MiB at
+ *                N = 2, 2 MiB above: rank j pulls slice j of every rank,
+ *                folds it with each element's color program and TMA-stores
+ *                the result into every rank's buffer (MD_AR_PUSH);
+ *   tree         everything else (fused updates, worker folds, unaligned
+ *                buffers): the pipelined per-color reduce + broadcast over
+ *                peer memory (or the owner plan, md_plan_set_schedule);
  *   stream       opt-in (MD_AR_STREAM=1): tiled all-pull with per-tile
  *                read-done flags.
  *
