@@ -91,7 +91,7 @@ def tree_config(n: int):
 
 class Clocks:
     """SM clock + throttle reasons of the run's GPUs, polled through NVML (the
-    library nvidia-smi reads) every ~1 ms by a thread during the timed region
+    library nvidia-smi reads) every ~0.2 ms by a thread during the timed region
     -- the region is milliseconds long, below nvidia-smi's sampling period."""
 
     REASONS = {  # NVML clocks-event bits -> the recipe's names
@@ -106,6 +106,7 @@ class Clocks:
         self.run = False
         self.err = None
         self.max_mhz = None
+        self.ready = threading.Event()
 
     def _loop(self):
         try:
@@ -114,20 +115,23 @@ class Clocks:
             nv.nvmlInit()
             hs = [nv.nvmlDeviceGetHandleByIndex(i) for i in self.gpus]
             self.max_mhz = max(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM) for h in hs)
+            self.ready.set()
             while self.run:
                 for h in hs:
                     self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
                     self.mask |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
-                time.sleep(0.001)
+                time.sleep(0.0002)  # the timed region can be ~2 ms long
             nv.nvmlShutdown()
         except Exception as e:  # noqa: BLE001
             self.err = repr(e)
+            self.ready.set()
 
     def start(self):
         self.run = True
         self.t = threading.Thread(target=self._loop, daemon=True)
         self.t.start()
-        time.sleep(0.05)  # NVML init before the timed region starts
+        self.ready.wait(timeout=30)  # NVML initialised (slow on multi-GPU boxes) before timing
+        time.sleep(0.005)
 
     def stop(self) -> dict:
         self.run = False
@@ -137,7 +141,7 @@ class Clocks:
         reasons = [k for k, bit in self.REASONS.items() if self.mask & bit]
         return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.sm),
-                "source": "NVML, 1 ms polling during the timed region"}
+                "source": "NVML, ~0.2 ms polling during the timed region"}
 
 
 # -- our implementation ------------------------------------------------------------------------------
