@@ -380,13 +380,14 @@ def run_ours(a) -> None:
                 "algorithmic_bytes_per_launch": 2 * P * 4 * (N - 1) / N,
                 "kernel": "md::allreduce_channels_kernel<4> (fused multicolor allreduce + SGD)"}
     else:
-        # lone rank: the fused kernel is the momentum/wd update: read g, r/w W and v
+        # lone rank: the allreduce is the identity and the fused call is the
+        # momentum/wd update (md_allreduce -> md_sgd_update): read g, r/w W and v
         algo_bytes = P * 20
         achieved = algo_bytes / (ar_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                 "frac": achieved / peak_hbm, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes,
-                "kernel": "md::allreduce_channels_kernel<4> (N=1: fused SGD momentum+wd epilogue)"}
+                "kernel": "md::sgd_vec_kernel<true,true> (N=1: identity allreduce + SGD momentum+wd update)"}
     roof["traffic"] = _ncu_traffic(N)
     line = {
         "metric": METRIC,

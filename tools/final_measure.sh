@@ -19,7 +19,7 @@ $R --nproc-per-node 4 --master-port 29609 bench_dimd.py > gpurun_out/F_d4.json 2
 MD_BENCH_NOCLOCK=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/F_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/F_ncu1.log 2>&1
-MD_BENCH_NOCLOCK=1 ncu --set full --clock-control none --import-source on -k regex:allreduce_channels_kernel \
+MD_BENCH_NOCLOCK=1 ncu --set full --clock-control none --import-source on -k regex:sgd_vec_kernel \
   -s 3 -c 1 -o gpurun_out/F_ar_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/F_ncu2.log 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/F_smi.txt
