@@ -139,7 +139,8 @@ int md_plan_set_schedule(md_plan_t* plan, int32_t schedule);
  *   owner-push   plain buffers (no fused update / worker fold) from 32 MiB at
  *                N = 2, 2 MiB above: rank j pulls slice j of every rank,
  *                folds it with each element's color program and TMA-stores
- *                the result into every rank's buffer (MD_AR_PUSH);
+ *                the result into every rank's buffer (MD_AR_PUSH; fused
+ *                updates opt-in with MD_AR_PUSH_FUSED=1, measured slower);
  *   tree         everything else (fused updates, worker folds, unaligned
  *                buffers): the pipelined per-color reduce + broadcast over
  *                peer memory (or the owner plan, md_plan_set_schedule);

@@ -1707,16 +1707,22 @@ __global__ void __launch_bounds__(kArThreads, 1)
   }
 }
 
-// ---- owner-push kernel (plain allreduce, large buffers) ---------------------------
+// ---- owner-push kernel (large buffers) ------------------------------------------
 // Owner-computes with a PUSHED broadcast: rank j pulls slice j of every rank
 // through a TMA ring, folds each element with its color program (same bits),
 // and TMA-bulk-stores the final tile into its own buffer AND every peer's --
-// no DOWN tasks, no per-segment flags: a peer only needs every push into its
-// buffer to have landed before the call returns, which the exit barrier's
-// done flag certifies (each CTA waited for its bulk stores to complete).
-// Pulls and pushes split the 2 (N-1)/N bytes per rank between the two
-// protocols (measured ceilings: pull ~650, push ~688 GB/s bidirectional).
-// No fused epilogue (the receivers would need per-tile arrival signals).
+// no DOWN tasks, no per-segment flag fences. Slices are 16-byte aligned (the
+// <= 3 trailing elements of the buffer go to the last owner, scalar).
+// Plain calls: a peer needs the pushes only at the end of the call, which the
+// exit barrier's done flag certifies (each CTA waited for its bulk stores to
+// complete). Fused SGD calls (kEpi != 0): the owner updates W / momentum of
+// its own slice in the fold warps, and once a tile's bulk stores have
+// COMPLETED (cp.async.bulk.wait_group, no system fence: the flag follows the
+// finished writes) the storer sets a per-tile "landed" flag in every peer's
+// control block (rd[owner][tile]); a quarter of each rank's CTAs are
+// receivers that wait for those flags and apply the update to the pushed
+// tiles from local memory. Pulls and pushes split the 2 (N-1)/N bytes per
+// rank between the two protocols (measured ceilings ~650 / ~688 GB/s).
 constexpr int kPushConsumerBase = 64;
 constexpr int kPushConsumerWarps = kArThreads / 32 - 2;
 
@@ -1725,21 +1731,51 @@ __device__ __forceinline__ void bulk_store_nc(void* gdst, const void* ssrc, uint
                "r"(smem_addr(ssrc)), "r"(bytes)
                : "memory");
 }
+// 16-byte aligned slice j of an n-element buffer (the tail n & 3 is not in any)
+__device__ __forceinline__ void push_slice(int64_t n, int N, int j, int64_t* lo, int64_t* hi) {
+  const int64_t n4 = n & ~int64_t(3);
+  const int64_t per = ((n4 / 4 + N - 1) / N) * 4;
+  *lo = min(n4, static_cast<int64_t>(j) * per);
+  *hi = min(n4, static_cast<int64_t>(j + 1) * per);
+}
+// SGD update of [lo, hi) (16-byte aligned lo) from g in `g` (global, L1 bypass)
+template <int kEpi>
+__device__ __forceinline__ void push_epilogue(const AllreduceArgs& a, const ViewArgs& v,
+                                              int64_t lo, int64_t hi, int t0, int nt) {
+  constexpr bool kMom = kEpi >= 3;
+  const int64_t ulen4 = a.update_len & ~int64_t(3);
+  for (int64_t i = lo + 4 * t0; i < hi; i += 4 * static_cast<int64_t>(nt)) {
+    if (i + 4 <= ulen4) {
+      const float4 g = __ldcg(reinterpret_cast<const float4*>(v.buf + i));
+      float4 w = __ldcs(reinterpret_cast<const float4*>(v.w + i));
+      float4 m = kMom ? __ldcs(reinterpret_cast<const float4*>(v.mom + i))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      sgd_elem<kEpi>(w.x, g.x, m.x, a);
+      sgd_elem<kEpi>(w.y, g.y, m.y, a);
+      sgd_elem<kEpi>(w.z, g.z, m.z, a);
+      sgd_elem<kEpi>(w.w, g.w, m.w, a);
+      __stcs(reinterpret_cast<float4*>(v.w + i), w);
+      if (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m);
+    } else {
+      for (int64_t q = i; q < min(hi, i + 4); ++q) epi_scalar<kEpi>(a, v, q, __ldcg(v.buf + q));
+    }
+  }
+}
 
+template <int kEpi>
 __global__ void __launch_bounds__(kArThreads, 1)
     allreduce_push_kernel(const __grid_constant__ AllreduceArgs a) {
   const int view = blockIdx.x / a.ctas_per_view;
   const int local_cta = blockIdx.x % a.ctas_per_view;
-  const int G = a.ctas_per_view;
+  const int G = a.max_stage;  // owner CTAs; local_cta >= G are receivers (fused only)
+  const int R = a.ctas_per_view - G;
   const ViewArgs& v = a.v[view];
   const int tid = threadIdx.x;
   const int N = a.n_ranks, me = v.rank;
   const int64_t TE = a.seg;
   const int S = a.lag;
-  int64_t s0, sl;
-  chunk_of(a.n, N, me, &s0, &sl);  // my slice
-  const int64_t A = min(s0 + sl, (s0 + 3) & ~int64_t(3));
-  const int64_t B = max(A, (s0 + sl) & ~int64_t(3));
+  int64_t A, B;
+  push_slice(a.n, N, me, &A, &B);
   const int64_t T = (B - A + TE - 1) / TE;
   const size_t slot_f = static_cast<size_t>(TE);
   const size_t stage_f = slot_f * (N + 1);  // [N rank slots][result]
@@ -1762,21 +1798,92 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __syncthreads();
   const uint32_t epoch = s_epoch;
   const bool ok = entry_barrier(a, v, local_cta, epoch);
-  if (ok) [&]() {
-    if (tid < 32) {  // ---------------- producer (+ the slice's unaligned edges) ----------------
-      if (tid != 0) return;
-      if (local_cta == 0) {
-        for (int64_t i = s0; i < s0 + sl; ++i) {
-          if (i >= A && i < B) {
-            i = B - 1;
-            continue;
+  if (ok && local_cta >= G) [&]() {  // ---------------- receiver (fused only) ----------------
+    // batches of kRB tiles of the other slices (tile-major, so early tiles
+    // come first); every thread keeps 3 x kRB 16-byte loads in flight
+    constexpr int kRB = 4;
+    constexpr bool kMom = kEpi >= 3;
+    const int64_t ulen4 = a.update_len & ~int64_t(3);
+    int64_t l0, h0;
+    push_slice(a.n, N, 0, &l0, &h0);
+    const int64_t np = ((h0 - l0 + TE - 1) / TE) * (N - 1);  // (tile, source) pairs
+    __shared__ int64_t s_lo[kRB], s_hi[kRB];
+    for (int64_t p0 = static_cast<int64_t>(local_cta - G) * kRB; p0 < np; p0 += static_cast<int64_t>(R) * kRB) {
+      if (tid < kRB) {
+        s_lo[tid] = s_hi[tid] = 0;
+        const int64_t p = p0 + tid;
+        if (p < np) {
+          const int64_t t = p / (N - 1);
+          int r = static_cast<int>(p % (N - 1));
+          r += r >= me;
+          int64_t lo, hi;
+          push_slice(a.n, N, r, &lo, &hi);
+          if (lo + t * TE < hi) {
+            s_lo[tid] = lo + t * TE;
+            s_hi[tid] = min(hi, lo + t * TE + TE);
+            const uint32_t* f = &v.ctrl->rd[r][t];
+            if (!epoch_ge(ld_relaxed_sys(f), epoch)) {
+              const uint64_t t0 = globaltimer_ns();
+              uint32_t sp = 0;
+              while (!epoch_ge(ld_relaxed_sys(f), epoch)) {
+                if ((++sp & 1023) == 0) {
+                  if (aborted(v)) { s_hi[tid] = s_lo[tid]; break; }
+                  if (globaltimer_ns() - t0 > a.timeout_ns) {
+                    raise_err(v, MD_ERR_TIMEOUT, 7000 + r);
+                    s_hi[tid] = s_lo[tid];
+                    break;
+                  }
+                }
+              }
+            }
           }
+        }
+      }
+      __syncthreads();
+      for (int64_t e = 4 * static_cast<int64_t>(tid); e < TE; e += 4 * static_cast<int64_t>(blockDim.x)) {
+        float4 g[kRB], w[kRB], m[kRB];
+        bool vec[kRB];
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) {
+          const int64_t i = s_lo[q] + e;
+          vec[q] = i + 4 <= s_hi[q] && i + 4 <= ulen4;
+          if (vec[q]) {
+            g[q] = __ldcg(reinterpret_cast<const float4*>(v.buf + i));
+            w[q] = __ldcs(reinterpret_cast<const float4*>(v.w + i));
+            m[q] = kMom ? __ldcs(reinterpret_cast<const float4*>(v.mom + i))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kRB; ++q) {
+          const int64_t i = s_lo[q] + e;
+          if (vec[q]) {
+            sgd_elem<kEpi>(w[q].x, g[q].x, m[q].x, a);
+            sgd_elem<kEpi>(w[q].y, g[q].y, m[q].y, a);
+            sgd_elem<kEpi>(w[q].z, g[q].z, m[q].z, a);
+            sgd_elem<kEpi>(w[q].w, g[q].w, m[q].w, a);
+            __stcs(reinterpret_cast<float4*>(v.w + i), w[q]);
+            if (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m[q]);
+          } else {
+            for (int64_t j = i; j < min(s_hi[q], i + 4); ++j) epi_scalar<kEpi>(a, v, j, __ldcg(v.buf + j));
+          }
+        }
+      }
+      __syncthreads();
+      if (aborted(v)) return;
+    }
+  }();
+  if (ok && local_cta < G) [&]() {
+    if (tid < 32) {  // ---------------- producer (+ the buffer's tail) ----------------
+      if (tid != 0) return;
+      if (me == N - 1 && local_cta == 0) {
+        for (int64_t i = a.n & ~int64_t(3); i < a.n; ++i) {  // <= 3 elements
           float x[MD_MAX_RANKS];
           for (int r = 0; r < N; ++r) x[r] = r == me ? v.buf[i] : v.peer[r][i];
           const float g = fold_prog(prog.c[color_of(a.n, a.k, i)], x, 1, 0);
           for (int r = 0; r < N; ++r) (r == me ? v.buf : const_cast<float*>(v.peer[r]))[i] = g;
         }
-        __threadfence_system();  // edge pushes are generic stores: visible before our done flag
+        __threadfence_system();  // tail pushes are generic stores: visible before our done flag
       }
       fence_proxy_async_global();
       uint32_t seq = 0;
@@ -1797,6 +1904,12 @@ __global__ void __launch_bounds__(kArThreads, 1)
     } else if (tid < kPushConsumerBase) {  // ---------------- storer ----------------
       if (tid != 32) return;
       uint32_t seq = 0;
+      int64_t tprev = -1, tprev2 = -1;  // tiles whose writes may still be in flight
+      auto landed = [&](int64_t t) {  // per-tile flags for the receivers
+        if (kEpi == 0 || t < 0) return;
+        for (int r = 0; r < N; ++r)
+          if (r != me) st_relaxed_sys(&v.peer_ctrl[r]->rd[me][t], epoch);
+      };
       for (int64_t t = local_cta; t < T; t += G, ++seq) {
         const uint32_t st = seq % S;
         uint32_t spins = 0;
@@ -1815,9 +1928,17 @@ __global__ void __launch_bounds__(kArThreads, 1)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[(seq - 1) % S]))
                        : "memory");
         }
+        if (kEpi != 0 && seq >= 2) {  // the tile before that has landed everywhere
+          asm volatile("cp.async.bulk.wait_group 2;" ::: "memory");
+          landed(tprev2);
+        }
+        tprev2 = tprev;
+        tprev = t;
       }
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every push has landed
-    } else {  // ---------------- fold ----------------
+      landed(tprev2);
+      landed(tprev);
+    } else {  // ---------------- fold (+ own slice's SGD update) ----------------
       const int ct = tid - kPushConsumerBase, nct = kPushConsumerWarps * 32;
       uint32_t seq = 0;
       for (int64_t t = local_cta; t < T; t += G, ++seq) {
@@ -1841,6 +1962,30 @@ __global__ void __launch_bounds__(kArThreads, 1)
         __syncwarp();
         if ((ct & 31) == 0)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&folded[st])) : "memory");
+        if constexpr (kEpi != 0) {  // own slice: W / momentum from the result in SMEM
+          constexpr bool kMom = kEpi >= 3;
+          const int64_t ulen4 = a.update_len & ~int64_t(3);
+          for (int64_t e = 4 * ct; e < len; e += 4 * nct) {
+            const int64_t i = lo + e;
+            const float4 g = *reinterpret_cast<const float4*>(res + e);
+            if (i + 4 <= ulen4) {
+              float4 w = __ldcs(reinterpret_cast<const float4*>(v.w + i));
+              float4 m = kMom ? __ldcs(reinterpret_cast<const float4*>(v.mom + i))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+              sgd_elem<kEpi>(w.x, g.x, m.x, a);
+              sgd_elem<kEpi>(w.y, g.y, m.y, a);
+              sgd_elem<kEpi>(w.z, g.z, m.z, a);
+              sgd_elem<kEpi>(w.w, g.w, m.w, a);
+              __stcs(reinterpret_cast<float4*>(v.w + i), w);
+              if (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m);
+            } else {
+              epi_scalar<kEpi>(a, v, i, g.x);
+              epi_scalar<kEpi>(a, v, i + 1, g.y);
+              epi_scalar<kEpi>(a, v, i + 2, g.z);
+              epi_scalar<kEpi>(a, v, i + 3, g.w);
+            }
+          }
+        }
       }
     }
   }();
@@ -2562,42 +2707,60 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     }
   }
 
-  // owner-push kernel: plain allreduce (no fused epilogue, no worker fold)
-  // from push_min_bytes(N) up; MD_AR_PUSH=0 disables it, =1 forces it
+  // owner-push kernel: plain buffers from push_min_bytes(N) up (MD_AR_PUSH=0
+  // disables it, =1 forces it); fused SGD calls opt-in (MD_AR_PUSH_FUSED=1)
+  // while the update range avoids the buffer's unaligned tail
   const char* pe = getenv("MD_AR_PUSH");
-  const bool push_want = pe ? atoi(pe) != 0 : n * 4 >= push_min_bytes(N);
-  if (push_want && epi == 0 && N > 1 && n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
+  const bool push_size = pe ? atoi(pe) != 0 : n * 4 >= push_min_bytes(N);
+  const bool push_fused = getenv("MD_AR_PUSH_FUSED") != nullptr;
+  if (push_size && (epi == 0 || (push_fused && update_len <= (n & ~int64_t(3)))) && N > 1 &&
+      n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
     int64_t TE = 4096;
     if (const char* te = getenv("MD_AR_TILE")) TE = std::max<int64_t>(4, atoll(te) & ~int64_t(3));
+    const int64_t n4 = n & ~int64_t(3);
+    const int64_t per = ((n4 / 4 + N - 1) / N) * 4;
+    while ((per + TE - 1) / TE > kMaxTiles) TE *= 2;
     const int64_t stage_bytes = static_cast<int64_t>(N + 1) * TE * 4;
     const int S = static_cast<int>(std::min<int64_t>(8, kRingBytes / stage_bytes));
     const int avail = sm_count(dev) / n_views;
-    if (S >= 2 && avail >= 1) {
-      int64_t mx_t = 1;
-      for (int j = 0; j < N; ++j) {
-        int64_t st0, ln;
-        chunk_of(n, N, j, &st0, &ln);
-        mx_t = std::max(mx_t, (ln + TE - 1) / TE);
+    if (S >= 2 && avail >= 2) {
+      const int64_t T = std::max<int64_t>(1, (per + TE - 1) / TE);
+      int recv = 0;
+      if (epi != 0) {
+        recv = avail / 4;
+        if (const char* rc = getenv("MD_AR_PUSH_RECV")) recv = atoi(rc);
+        recv = std::max(1, std::min(recv, avail - 1));
       }
-      const int g = static_cast<int>(std::min<int64_t>(avail, mx_t));
+      const int g_own = static_cast<int>(std::min<int64_t>(avail - recv, T));
       a.seg = TE;
       a.lag = S;
-      a.ctas_per_view = g;
+      a.max_stage = g_own;
+      a.ctas_per_view = g_own + recv;
       a.prog = plan->prog_dev;
-      const void* pk = (const void*)allreduce_push_kernel;
+      const void* pk = nullptr;
+      switch (epi) {
+        case 1: pk = (const void*)allreduce_push_kernel<1>; break;
+        case 2: pk = (const void*)allreduce_push_kernel<2>; break;
+        case 3: pk = (const void*)allreduce_push_kernel<3>; break;
+        case 4: pk = (const void*)allreduce_push_kernel<4>; break;
+        default: pk = (const void*)allreduce_push_kernel<0>; break;
+      }
       static std::atomic<uint32_t> pk_set[64];
-      if (dev < 0 || dev >= 64 || !pk_set[dev].exchange(1)) {
+      const uint32_t pbit = 1u << epi;
+      if (dev < 0 || dev >= 64 || !(pk_set[dev].load() & pbit)) {
         MD_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(kRingBytes)));
+        if (dev >= 0 && dev < 64) pk_set[dev].fetch_or(pbit);
       }
       const size_t smem = static_cast<size_t>(S) * stage_bytes;
+      const unsigned grid = static_cast<unsigned>(a.ctas_per_view);
       void* args[] = {&a};
       if (n_views > 1 || getenv("MD_AR_COOP")) {
-        MD_CUDA_TRY(cudaLaunchCooperativeKernel(pk, dim3(static_cast<unsigned>(g) * n_views),
-                                                dim3(kArThreads), args, smem, as_stream(stream)));
+        MD_CUDA_TRY(cudaLaunchCooperativeKernel(pk, dim3(grid * n_views), dim3(kArThreads), args,
+                                                smem, as_stream(stream)));
       } else {
-        MD_CUDA_TRY(cudaLaunchKernel(pk, dim3(static_cast<unsigned>(g)), dim3(kArThreads), args,
-                                     smem, as_stream(stream)));
+        MD_CUDA_TRY(cudaLaunchKernel(pk, dim3(grid), dim3(kArThreads), args, smem,
+                                     as_stream(stream)));
       }
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return MD_OK;

@@ -25,20 +25,25 @@ from tests.test_oracle import GOLD_MC
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream", "push"])
+@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream", "push", "pushfused"])
 def ar_path(request, monkeypatch):
     """Every test runs on each kernel: the pipelined tree schedule
     (allreduce_channels_kernel / the work-queue kernel), the one-shot pull
     kernel, the LL push kernel, the tiled all-pull stream kernel and the
-    owner-push kernel -- the last four evaluate the same fold programs
-    locally, so the bits must not change. (Calls a path cannot take -- fused
-    epilogues for push, sizes beyond a path's range -- fall through to the
-    tree schedule.)"""
+    owner-push kernel (plain, and with the fused SGD update on receiver CTAs)
+    -- all but the tree evaluate the same fold programs locally, so the bits
+    must not change. (Calls a path cannot take -- worker folds, sizes beyond
+    a path's range -- fall through to the tree schedule.)"""
     big = str(1 << 40)
-    monkeypatch.setenv("MD_AR_ONESHOT_MAX", big if request.param == "oneshot" else "0")
-    monkeypatch.setenv("MD_AR_LL_MAX", big if request.param == "ll" else "0")
-    monkeypatch.setenv("MD_AR_STREAM", "1" if request.param == "stream" else "0")
-    monkeypatch.setenv("MD_AR_PUSH", "1" if request.param == "push" else "0")
+    p = request.param
+    monkeypatch.setenv("MD_AR_ONESHOT_MAX", big if p == "oneshot" else "0")
+    monkeypatch.setenv("MD_AR_LL_MAX", big if p == "ll" else "0")
+    monkeypatch.setenv("MD_AR_STREAM", "1" if p == "stream" else "0")
+    monkeypatch.setenv("MD_AR_PUSH", "1" if p in ("push", "pushfused") else "0")
+    if p == "pushfused":
+        monkeypatch.setenv("MD_AR_PUSH_FUSED", "1")
+    else:
+        monkeypatch.delenv("MD_AR_PUSH_FUSED", raising=False)
     return request.param
 
 
@@ -109,6 +114,7 @@ def test_oneshot_and_tree_calls_interleave(oracle, monkeypatch):
     monkeypatch.delenv("MD_AR_LL_MAX", raising=False)
     monkeypatch.delenv("MD_AR_STREAM", raising=False)
     monkeypatch.delenv("MD_AR_PUSH", raising=False)
+    monkeypatch.delenv("MD_AR_PUSH_FUSED", raising=False)
     n = 4
     ts = build_multicolor_trees(n, 4, 4)
     tables = oracle.tables_from_trees(n, oracle.trees(n, 4, 4))
@@ -129,6 +135,39 @@ def test_oneshot_and_tree_calls_interleave(oracle, monkeypatch):
 
     for r in run_ranks(n, "cuda", prog, emulate=True).results:
         assert all(r)
+
+
+@pytest.mark.parametrize("n,k,arity", [(2, 2, 4), (4, 4, 4), (8, 4, 4)])
+@pytest.mark.parametrize("tail_in_update", [False, True])
+def test_fused_update_without_workers(oracle, n, k, arity, tail_in_update):
+    """Allreduce + momentum/wd update, no worker fold: the fused path of every
+    kernel (tree epilogue, owner-push own slice + receiver CTAs). A 2.5M + 2
+    float buffer; the update covers everything but the 2-element tail, or the
+    tail too (then owner-push must hand the call to the tree)."""
+    rng = np.random.default_rng(n * 7 + k + int(tail_in_update))
+    L = 2_500_002
+    P = L - 1 if tail_in_update else L - 2
+    arrays = [rng.standard_normal(L).astype(np.float32) for _ in range(n)]
+    w0 = rng.standard_normal(P).astype(np.float32)
+    m0 = rng.standard_normal(P).astype(np.float32)
+    tables = oracle.tables_from_trees(n, oracle.trees(n, k, arity))
+    want = oracle.fold_c(tables, arrays)
+    want_w, want_m = oracle.sgd_np(w0, want[:P], m0.copy(), 1e-3, 0.9, 3.2e-3)
+    ts = build_multicolor_trees(n, k, arity)
+
+    def prog(ep):
+        dev = ep.torch_device
+        buf = GradientBuffer(torch.from_numpy(arrays[ep.rank].copy()).to(dev))
+        w = torch.from_numpy(w0.copy()).to(dev)
+        m = torch.from_numpy(m0.copy()).to(dev)
+        upd = SgdUpdate(weights=w, c=1e-3, momentum=m, mu=0.9, wd_b=3.2e-3, update_len=P)
+        allreduce(ep, buf, "multicolor", tree_set=ts, update=upd)
+        return buf.data.cpu().numpy(), w.cpu().numpy(), m.cpu().numpy()
+
+    for g, w, m in run_ranks(n, "cuda", prog, emulate=True).results:
+        assert np.array_equal(g, want)
+        assert np.array_equal(w, want_w)
+        assert np.array_equal(m, want_m)
 
 
 def test_host_numpy_buffers_are_a_drop_in(golden):
