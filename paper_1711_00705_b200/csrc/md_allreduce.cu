@@ -2715,7 +2715,9 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   const bool push_fused = getenv("MD_AR_PUSH_FUSED") != nullptr;
   if (push_size && (epi == 0 || (push_fused && update_len <= (n & ~int64_t(3)))) && N > 1 &&
       n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
-    int64_t TE = 4096;
+    // tile: deep enough rings for the N sources (measured, graph-timed 1 GiB:
+    // N = 4 2048 -> 2361 us vs 4096 -> 2596 us; N = 2 3072 -> 1615 vs 1636)
+    int64_t TE = N == 2 ? 3072 : 2048;
     if (const char* te = getenv("MD_AR_TILE")) TE = std::max<int64_t>(4, atoll(te) & ~int64_t(3));
     const int64_t n4 = n & ~int64_t(3);
     const int64_t per = ((n4 / 4 + N - 1) / N) * 4;
