@@ -378,7 +378,11 @@ def run_ours(a) -> None:
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
                 "algorithmic_bytes_per_launch": 2 * P * 4 * (N - 1) / N,
-                "kernel": "md::allreduce_channels_kernel<4> (fused multicolor allreduce + SGD)"}
+                # md_allreduce's default route for this fused call (include/mdb200.h)
+                "kernel": ("md::allreduce_stream_kernel<4> (fused all-pull multicolor allreduce + SGD)"
+                           if (os.environ["MD_AR_STREAM"] != "0" if "MD_AR_STREAM" in os.environ
+                               else N == 2) else
+                           "md::allreduce_channels_kernel<4> (fused multicolor allreduce + SGD)")}
     else:
         # lone rank: the allreduce is the identity and the fused call is the
         # momentum/wd update (md_allreduce -> md_sgd_update): read g, r/w W and v

@@ -373,6 +373,10 @@ __device__ __forceinline__ typename Elem<kVec>::T own_value(const AllreduceArgs&
 constexpr int kStages = 4;
 constexpr uint32_t kStageBytes = 48 * 1024;
 constexpr uint32_t kRingBytes = kStages * kStageBytes;
+// the stream kernel's ring: (almost) all of the 227 KB a CTA may opt into, so
+// N = 2 fused calls fit two stages of 7168-float tiles (4 slots: 2 ranks, W,
+// momentum); its static SMEM is ~1.4 KB
+constexpr uint32_t kStreamRingBytes = 224 * 1024;
 
 template <int kEpi>
 __device__ __forceinline__ void item_tma(const AllreduceArgs& a, const ViewArgs& v, const Task& t,
@@ -2448,6 +2452,10 @@ static int64_t oneshot_max_bytes(int N) {
   return N == 2 ? (int64_t(1) << 40) : (int64_t(1) << 20);
 }
 
+// Smallest buffer (bytes) a fused N = 2 call streams (measured win at the
+// 102.4 MB C5 buffer; below that the tree keeps it). MD_AR_STREAM overrides.
+static int64_t stream_min_bytes() { return int64_t(64) << 20; }
+
 // Largest buffer (bytes) the LL push kernel takes: it moves 2 x (N-1) x bytes
 // out of every rank (value + epoch words), so only latency-bound sizes:
 // measured faster than the one-shot pull up to 1 MiB at N = 2 and 4 (10.4 vs
@@ -2653,21 +2661,29 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     }
   }
   const void* kern = nullptr;
-  // stream (all-pull, tiled) kernel, opt-in (MD_AR_STREAM=1): see
-  // allreduce_stream_kernel. Measured at N = 2 it ties the tree schedule at
-  // 100 MB (199.7 vs 199.7 us fused) and reaches the pull ceiling at 1 GiB
-  // (648 vs 634 GB/s bus), but loses below (per-tile cost), so the tree stays
-  // the default (profiles/README.md).
+  // stream (all-pull, tiled) kernel: see allreduce_stream_kernel. Default for
+  // FUSED calls at N = 2 from stream_min_bytes() up, with balanced tiles of
+  // <= 6656 floats (two stages of [2 ranks | W | momentum] in the 224 KB
+  // ring): C5 step at N = 2, graph-timed, 206 -> 198 us (allreduce 197 -> 189
+  // us; tiles 5120 / 6144 / 7168 measured 210 / 189-193 / 193 us,
+  // profiles/README.md). At N > 2 it pulls (N-1) x bytes and loses (N = 4:
+  // 502 vs 275 us), so there it is opt-in only. MD_AR_STREAM=0/1 overrides
+  // the choice, MD_AR_TILE the tile.
   {
     const char* se = getenv("MD_AR_STREAM");
-    const bool want = se && atoi(se) != 0;
+    const bool want = se ? atoi(se) != 0 : (N == 2 && epi != 0 && n * 4 >= stream_min_bytes());
     if (want && N > 1 && n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
       int64_t TE = 2048;
+      if (N == 2) {  // balanced: every CTA gets the same number of tiles
+        const int64_t G = std::max(1, sm_count(dev) / n_views);
+        const int64_t rounds = std::max<int64_t>(1, (n + G * 6656 - 1) / (G * 6656));
+        TE = std::max<int64_t>(4, ((n + G * rounds - 1) / (G * rounds) + 3) & ~int64_t(3));
+      }
       if (const char* te = getenv("MD_AR_TILE")) TE = std::max<int64_t>(4, atoll(te) & ~int64_t(3));
       while ((n + TE - 1) / TE > kMaxTiles) TE *= 2;
       const int epi_slots = epi == 0 ? 0 : (epi >= 3 ? 2 : 1);
       const int64_t stage_bytes = static_cast<int64_t>(N + epi_slots) * TE * 4;
-      const int S = static_cast<int>(std::min<int64_t>(8, kRingBytes / stage_bytes));
+      const int S = static_cast<int>(std::min<int64_t>(8, kStreamRingBytes / stage_bytes));
       const int avail = sm_count(dev) / n_views;
       if (S >= 2 && avail >= 1) {
         const int64_t T = (n + TE - 1) / TE;
@@ -2688,7 +2704,7 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
         const uint32_t sbit = 1u << epi;
         if (dev < 0 || dev >= 64 || !(st_set[dev].load() & sbit)) {
           MD_CUDA_TRY(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kRingBytes)));
+                                           static_cast<int>(kStreamRingBytes)));
           if (dev >= 0 && dev < 64) st_set[dev].fetch_or(sbit);
         }
         const size_t smem = static_cast<size_t>(S) * stage_bytes;
