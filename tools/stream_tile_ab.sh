@@ -8,6 +8,6 @@ run() {  # label n env...
   python -c "import json; d=json.load(open('$out')); print('N=$n $label', round(d['step_ms']*1000,2), 'us/step', round(d['allreduce']['ms']*1000,2), 'us ar', round(d['roofline']['frac'],3))" || tail -5 $out.err
 }
 for rep in a b; do
-  run tree$rep 2 X=1
+  run tree$rep 2 MD_AR_STREAM=0
   for t in ${TILES:-5120 6144 6656 7168}; do run stream$t$rep 2 MD_AR_STREAM=1 MD_AR_TILE=$t; done
 done
