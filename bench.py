@@ -67,6 +67,12 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly")
+    ap.add_argument("--update", choices=["replicated", "sharded"], default="replicated",
+                    help="SGD update mode of the fused call (SgdUpdate.sharded): every rank "
+                         "updates its replica, or the owner of each slice updates it and pushes "
+                         "the new weights (same bits)")
+    ap.add_argument("--nvlink-reps", type=int, default=40,
+                    help="replays of the allreduce graph inside the NVLink-counter window")
     return ap.parse_args()
 
 
@@ -174,13 +180,14 @@ def run_ours(a) -> None:
         store = dimd.synth_store(SHARD, REC, rank, N, SEED, 0, N, rank, device=dev)
         g = torch.Generator(device=dev)
         g.manual_seed(SEED)  # identical replicas on every rank
-        w = torch.randn(P, generator=g, device=dev) * 0.01
+        w, _ = ep.alloc(P)  # peer-registered (the sharded update pushes into it)
+        w.copy_(torch.randn(P, generator=g, device=dev) * 0.01)
         model = DeviceModel(w, torch.zeros_like(w))
         grad = GradientBuffer.alloc(P + 2, ep)
         slots = BatchSlots(BATCH, REC, dev)
         batches = BatchStream(store, BATCH, REC, SEED, SAMPLE_ROLE, rank)  # device step counter
         upd = SgdUpdate(weights=model.weights, c=lr / B, momentum=model.momentum, mu=MOM,
-                        wd_b=WD * B, update_len=P)
+                        wd_b=WD * B, update_len=P, sharded=a.update == "sharded")
     torch.cuda.synchronize(dev)
 
     def fill():
@@ -301,6 +308,24 @@ def run_ours(a) -> None:
             torch.cuda.synchronize(dev)
             ep.take_error()
         ar_ms = sum(e0.elapsed_time(e1) for e0, e1 in ar_ev) / len(ar_ev)
+        route = _lib.last_route(ep.device)  # the kernel md_allreduce picked for the step
+        # live NVLink bytes (NVML GPM link counters, no profiler): the serial
+        # schedule replayed back to back; only the allreduce touches NVLink
+        link = None
+        if N > 1 and graph is not None and a.nvlink_reps > 0:
+            from tools.linkmon import LinkMonitor
+
+            mon = LinkMonitor.create(ep.device)
+            if mon is not None:
+                ep.barrier()
+                torch.cuda.synchronize(dev)
+                mon.start()
+                for _ in range(a.nvlink_reps):
+                    graph_ar.replay()
+                torch.cuda.synchronize(dev)
+                link = mon.stop()
+                link["allreduce_calls"] = a.nvlink_reps * a.steps
+                ep.take_error()
         if os.environ.get("MD_BENCH_DEBUG"):
             print(json.dumps({"rank": rank, "ar_ms": [round(e0.elapsed_time(e1), 4)
                                                       for e0, e1 in ar_ev]}), file=sys.stderr)
@@ -361,7 +386,7 @@ def run_ours(a) -> None:
             e2e_ms = s0.elapsed_time(s1)
             e2e = (e2e_ms, (P + 2) * 4, 2 * 4 + BATCH * 4)
 
-    rows = ep.all_gather((ms, ar_ms, launches, e2e))
+    rows = ep.all_gather((ms, ar_ms, launches, e2e, link))
     if rank != 0:
         return
     ms = max(r[0] for r in rows)
@@ -371,6 +396,14 @@ def run_ours(a) -> None:
     value = N * BATCH / (step_ms / 1e3)
     bus = 2.0 * P * 4 * (N - 1) / N / (ar_ms / 1e3) / 1e9 if N > 1 else None
     peak_hbm, peak_src = hbm_peak()
+    kernels = {"stream": "md::allreduce_stream_kernel<4> (fused all-pull multicolor allreduce + SGD)",
+               "tree": "md::allreduce_channels_kernel<4> (fused multicolor allreduce + SGD)",
+               "queue": "md::allreduce_kernel<4> (work-queue multicolor allreduce + SGD)",
+               "push": "md::allreduce_push_kernel<4> (owner-push multicolor allreduce + "
+                       "sharded SGD, W' pushed)",
+               "local": "md::sgd_vec_kernel<true,true> (N=1: identity allreduce + SGD "
+                        "momentum+wd update)"}
+    kernel = kernels.get(route[0], route[0])
     if N > 1:
         achieved = bus
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK, "unit": "GB/s",
@@ -378,11 +411,9 @@ def run_ours(a) -> None:
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction",
                 "algorithmic_bytes_per_launch": 2 * P * 4 * (N - 1) / N,
-                # md_allreduce's default route for this fused call (include/mdb200.h)
-                "kernel": ("md::allreduce_stream_kernel<4> (fused all-pull multicolor allreduce + SGD)"
-                           if (os.environ["MD_AR_STREAM"] != "0" if "MD_AR_STREAM" in os.environ
-                               else N == 2) else
-                           "md::allreduce_channels_kernel<4> (fused multicolor allreduce + SGD)")}
+                # the route md_allreduce reported for the timed calls (md_last_route)
+                "kernel": kernel, "route": {"name": route[0], "tile": route[1],
+                                            "sharded": route[2]}}
     else:
         # lone rank: the allreduce is the identity and the fused call is the
         # momentum/wd update (md_allreduce -> md_sgd_update): read g, r/w W and v
@@ -390,9 +421,9 @@ def run_ours(a) -> None:
         achieved = algo_bytes / (ar_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                 "frac": achieved / peak_hbm, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": algo_bytes,
-                "kernel": "md::sgd_vec_kernel<true,true> (N=1: identity allreduce + SGD momentum+wd update)"}
-    roof["traffic"] = _ncu_traffic(N)
+                "algorithmic_bytes_per_launch": algo_bytes, "kernel": kernel,
+                "route": {"name": route[0], "tile": route[1], "sharded": route[2]}}
+    roof["traffic"], roof["traffic_source"] = _ncu_traffic(N, route)
     line = {
         "metric": METRIC,
         "value": value,
@@ -421,7 +452,9 @@ def run_ours(a) -> None:
         },
         "allreduce": {"ms": ar_ms, "bus_gbps": bus,
                       "frac_of_770": (bus / NVLINK_PEAK) if bus else None,
-                      "frac_of_900": (bus / NVLINK_NOMINAL) if bus else None},
+                      "frac_of_900": (bus / NVLINK_NOMINAL) if bus else None,
+                      "update": a.update},
+        "nvlink": _link_summary(rows, N, ar_ms),
         "roofline": roof,
         "gpu_launches": launches,
         "clocks": clk,
@@ -431,7 +464,7 @@ def run_ours(a) -> None:
         line["e2e"] = {"value": N * BATCH / (e2e_ms / 1e3), "unit": "samples/s",
                        "ms_per_step": e2e_ms, "h2d_bytes_per_step": e2e[1],
                        "d2h_bytes_per_step": e2e[2]}
-    if N == 1 and not a.no_cpu_baseline:
+    if not a.no_cpu_baseline:  # rank 0, after the GPU timing, bounded sample
         line["cpu_baseline"] = cpu_baseline_port(N)
     print(json.dumps(line), flush=True)
 
@@ -441,12 +474,41 @@ def _host_fill(n: int, rank: int, n_ranks: int) -> np.ndarray:
     return ((np.arange(n, dtype=np.float64) % 997.0 + 1.0) * scale).astype(np.float32)
 
 
-def _ncu_traffic(n: int):
+def _ncu_traffic(n: int, route):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernel
+    that ran, from the committed `ncu --set full` capture of the same command
+    (profiles/traffic.json names the capture); null when no capture of this
+    route at this N exists."""
     f = ROOT / "profiles" / "traffic.json"
     try:
-        return json.loads(f.read_text()).get(str(n))
+        rec = json.loads(f.read_text()).get(f"{n}:{route[0]}")
     except Exception:  # noqa: BLE001
+        rec = None
+    if not rec:
+        return None, None
+    return rec["bytes"], rec["source"]
+
+
+def _link_summary(rows, n: int, ar_ms: float):
+    """NVLink bytes per allreduce call from the GPM counters of every rank."""
+    if n == 1:
         return None
+    links = [r[4] for r in rows]
+    if any(x is None or "error" in x for x in links):
+        return {"error": "NVML GPM counters unavailable",
+                "detail": [x.get("error") if x else None for x in links]}
+    calls = links[0]["allreduce_calls"]
+    rx = [x["rx_bytes"] / calls for x in links]
+    tx = [x["tx_bytes"] / calls for x in links]
+    algo = 2 * P * 4 * (n - 1) / n  # per rank and direction, ref src/bench.py:116-119
+    return {"source": "NVML GPM NVLINK_TOTAL_{RX,TX}_PER_SEC x window, every rank, "
+                      "serial step schedule replayed back to back (only the allreduce "
+                      "uses NVLink)",
+            "rx_bytes_per_call": rx, "tx_bytes_per_call": tx,
+            "algorithmic_bytes_per_call_per_direction": algo,
+            "rx_over_algorithmic": max(rx) / algo,
+            "rx_gbps_while_allreduce": max(rx) / (ar_ms / 1e3) / 1e9,
+            "link_peak_gbps": NVLINK_NOMINAL}
 
 
 # -- CPU baseline / reference arm (oracle port) -------------------------------------------------------
@@ -463,8 +525,7 @@ def cpu_step_port(n_ranks: int, state: dict, step: int, threads: int) -> None:
         picks = O.integers_c(O.mix64(SEED, O.SAMP_ROLE, r, step), SHARD, BATCH)
         src = state["shard"]
         for j, pk in enumerate(picks):
-            k = int(pk) % state["shard_n"]  # bounded host shard (see sample text)
-            state["batch"][j] = src[k]
+            state["batch"][j] = src[int(pk)]
         _par_fill(L, state["grads"][r], r, n_ranks, threads)
     O.allreduce_threads(state["tables"], state["grads"], weights=state["w"], moms=state["v"],
                         update_len=P, c=state["c"], mu=MOM, wd_b=state["wd_b"], threads=threads)
@@ -508,13 +569,15 @@ def _cpu_state(n_ranks: int):
                       momentum=MOM, weight_decay=WD, base_lr=BASE_LR, seed=SEED)
     B = cfg.effective_batch
     rng = np.random.default_rng(SEED)
-    shard_n = 512
+    shard_n = SHARD
     return {
         "tables": tables,
         "grads": [np.zeros(P + 2, np.float32) for _ in range(n_ranks)],
         "w": [(rng.standard_normal(P, dtype=np.float32) * 0.01) for _ in range(1)] * n_ranks,
         "v": [np.zeros(P, np.float32) for _ in range(n_ranks)],
-        "shard": rng.integers(0, 256, size=(shard_n, REC), dtype=np.uint8),
+        # the GPU arm's shard size; calloc'd, so only the records a step
+        # gathers are ever backed by memory (24 GB would not fit a host)
+        "shard": np.zeros((shard_n, REC), dtype=np.uint8),
         "shard_n": shard_n,
         "batch": np.empty((BATCH, REC), np.uint8),
         "c": float(np.float32(lr_at(lr_schedule(cfg), 10.0) / B)),
@@ -537,8 +600,8 @@ def cpu_baseline_port(n_ranks: int, seconds: float = 10.0, min_steps: int = 3) -
     return {"value": n_ranks * BATCH / dt, "unit": "samples/s", "cores": threads, "kind": "port",
             "ms_per_step": dt * 1e3,
             "sample": f"{steps} full C5 steps for {n_ranks} rank(s) on the host: 32-record gather "
-                      f"(picks from the reference Philox stream, records from a 512-record host "
-                      f"shard), deterministic gradient fill, tree-order fold + broadcast + fused "
+                      f"(picks from the reference Philox stream over the same {SHARD}-record shard "
+                      f"as the GPU arm), deterministic gradient fill, tree-order fold + broadcast + fused "
                       f"SGD(momentum, wd) over 25.6M floats per rank (oracle/mdoracle.c, "
                       f"{threads} threads)"}
 
@@ -559,7 +622,8 @@ def run_reference(a) -> None:
     dt = (time.perf_counter() - t0) / a.steps
     v = N * BATCH / dt
     sample = (f"C5 step for all {N} ranks emulated on the host (rank 0 only): picks from the "
-              f"reference Philox stream, 32 x 150528-byte record gather per rank, gradient fill, "
+              f"reference Philox stream over the {SHARD}-record shard, 32 x 150528-byte record "
+              f"gather per rank, gradient fill, "
               f"tree-order multicolor fold + broadcast, fused SGD(momentum, wd) of 25.6M floats "
               f"per rank; oracle/mdoracle.c C port of the reference algorithm, {threads} threads")
     print(json.dumps({

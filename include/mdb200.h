@@ -124,27 +124,49 @@ int md_plan_destroy(md_plan_t* plan);
 #define MD_SCHED_OWNER 1
 int md_plan_set_schedule(md_plan_t* plan, int32_t schedule);
 
+/* Kernel route of md_allreduce for this plan (never changes the bits; see
+ * md_allreduce for what each one does). MD_ROUTE_AUTO picks by size, world
+ * size and update mode; any other value forces that route where it applies
+ * (a route that cannot serve a call -- e.g. LL with a worker fold, owner-push
+ * with a replicated update -- falls back to MD_ROUTE_TREE).
+ * tile: elements per tile of the tiled routes (stream, push); 0 = auto.
+ * The environment variable MD_AR_ROUTE=tree|queue|ll|oneshot|stream|push
+ * (read once per process) sets the default for plans left on AUTO. */
+#define MD_ROUTE_AUTO 0
+#define MD_ROUTE_TREE 1    /* channelized pipelined tree (or owner plan)     */
+#define MD_ROUTE_QUEUE 2   /* work-queue tree kernel (scalar path, any alignment) */
+#define MD_ROUTE_LL 3      /* LL push                                         */
+#define MD_ROUTE_ONESHOT 4 /* one-shot pull                                   */
+#define MD_ROUTE_STREAM 5  /* tiled all-pull with per-tile read-done flags    */
+#define MD_ROUTE_PUSH 6    /* owner-push (plain calls and sharded updates)    */
+#define MD_ROUTE_LOCAL 7   /* (reported only) N = 1: update kernel alone      */
+int md_plan_set_route(md_plan_t* plan, int32_t route, int64_t tile);
+/* Route (MD_ROUTE_*), tile/segment and update mode (1 = sharded) of the
+ * last md_allreduce launched on `device` by this process. */
+int md_last_route(int32_t device, int32_t* route, int64_t* tile, int32_t* sharded);
+
 /* ---- allreduce: collectives.py:225-296 (multicolor), :302-359 (ring),
  *      :365-409 (reduce_then_broadcast); dispatcher :412-429 ----------------- */
 /* One persistent kernel per call. `n_views` ranks are served by this call:
  * 1 for a real rank (one GPU per rank), n_ranks when every rank of the
  * world is emulated on one GPU (then comms[v] is rank v's communicator).
- * The kernel is picked by size; all of them produce the same bits (the plan's
- * fold order per color), which the GPU tests check for every path:
+ * The kernel is picked by size (md_plan_set_route overrides); all of them
+ * produce the same bits (the plan's fold order per color), which the GPU
+ * tests check for every path:
  *   LL push      n*4 <= 1 MiB (N <= 4; 256 KiB above): every rank pushes
  *                (value, epoch) words into its peers' control-block inbox and
  *                folds locally -- one NVLink trip, no barrier (MD_AR_LL_MAX);
  *   one-shot     N = 2 up to one SMEM pass of every rank's data (~14 MB):
  *                pull every peer buffer, fold locally (MD_AR_ONESHOT_MAX);
  *   owner-push   plain buffers (no fused update / worker fold) from 32 MiB at
- *                N = 2, 2 MiB above: rank j pulls slice j of every rank,
+ *                N = 2, 2 MiB above, and every SHARDED update
+ *                (md_allreduce_ex): rank j pulls slice j of every rank,
  *                folds it with each element's color program and TMA-stores
- *                the result into every rank's buffer (MD_AR_PUSH; fused
- *                updates opt-in with MD_AR_PUSH_FUSED=1, measured slower);
- *   stream       fused SGD updates at N = 2 from 64 MiB (opt-in elsewhere,
- *                MD_AR_STREAM=0/1 overrides): tiled all-pull through a TMA
- *                ring with per-tile read-done flags, balanced <= 6656-float
- *                tiles (C5 step 206 -> 198 us);
+ *                the result (or, sharded, the updated weights) into every
+ *                rank's buffer;
+ *   stream       replicated fused SGD updates at N = 2 from 64 MiB: tiled
+ *                all-pull through a TMA ring with per-tile read-done flags,
+ *                balanced <= 6656-float tiles (C5 step 206 -> 198 us);
  *   tree         everything else (fused updates, worker folds, unaligned
  *                buffers): the pipelined per-color reduce + broadcast over
  *                peer memory (or the owner plan, md_plan_set_schedule).
@@ -162,11 +184,40 @@ int md_plan_set_schedule(md_plan_t* plan, int32_t schedule);
  *             on the first update_len elements once the sum is final.
  *   seg_elems pipeline granularity (elements); results do not depend on it
  *             (pkg/tests/test_collectives.py:131-147).
- *   ctas      CTAs per view (0 = auto). */
+ *   ctas      CTAs per view (0 = auto).
+ * Every rank must take the same route with the same geometry; the entry
+ * barrier compares a route word across ranks and fails every rank with
+ * MD_ERR_INVALID_CONFIG if they differ (e.g. one rank's buffers misaligned). */
 int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan,
                  float* const* bufs, int64_t n, const float* const* workers, int32_t n_workers,
                  float* const* w, float* const* mom, int64_t update_len, float c, float mu,
                  float wd_b, int64_t seg_elems, int32_t ctas, void* stream);
+
+/* Fused SGD epilogue of md_allreduce_ex (md_sgd_update semantics on the
+ * first `len` elements once the sum is final).
+ *   MD_UPDATE_REPLICATED: w, mom are [n_views]; every rank updates its full
+ *     replica (the reference's replicated weights, sgd.py:416).
+ *   MD_UPDATE_SHARDED: w is [n_views * n_ranks] (view v, rank r: rank r's
+ *     weights as addressable from this process -- peer-mapped), mom is
+ *     [n_views]. The owner of each buffer slice updates it and pushes the
+ *     new weights into every rank (same bits: replicas are identical,
+ *     sgd.py:5-10); momentum is sharded state (only the own slice is read and
+ *     written) and the buffer holds the sum only on the own slice and past
+ *     `len`. Needs n_ranks > 1, no worker fold, 16-byte aligned buffers and
+ *     len % 4 == 0; otherwise the call runs replicated (a superset: same
+ *     weights, full sum, full momentum). */
+#define MD_UPDATE_REPLICATED 0
+#define MD_UPDATE_SHARDED 1
+typedef struct md_update {
+  float* const* w;
+  float* const* mom;
+  int64_t len;
+  float c, mu, wd_b;
+  int32_t mode;
+} md_update_t;
+int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan,
+                    float* const* bufs, int64_t n, const float* const* workers, int32_t n_workers,
+                    const md_update_t* update, int64_t seg_elems, int32_t ctas, void* stream);
 
 /* Diagnostics: with MD_AR_TRACE=1 in the environment every md_allreduce
  * records %globaltimer events per CTA (flag waits, chunk arrival, segment

@@ -23,6 +23,20 @@ MD_SCHED_TREE = 0   # md_plan_set_schedule: per-color trees (the reference's sch
 MD_SCHED_OWNER = 1  # owner-computes slices, same bits
 MD_MAX_GROUP = 64
 IPC_BYTES = 64
+# md_plan_set_route / md_last_route (include/mdb200.h)
+ROUTES = {"auto": 0, "tree": 1, "queue": 2, "ll": 3, "oneshot": 4, "stream": 5, "push": 6,
+          "local": 7}
+ROUTE_NAMES = {v: k for k, v in ROUTES.items()}
+MD_UPDATE_REPLICATED = 0
+MD_UPDATE_SHARDED = 1
+
+
+class MdUpdate(C.Structure):
+    """md_update_t (include/mdb200.h)."""
+
+    _fields_ = [("w", C.POINTER(C.c_void_p)), ("mom", C.POINTER(C.c_void_p)),
+                ("len", C.c_int64), ("c", C.c_float), ("mu", C.c_float), ("wd_b", C.c_float),
+                ("mode", C.c_int32)]
 
 _vp = C.c_void_p
 _i32 = C.c_int32
@@ -59,9 +73,14 @@ SIGNATURES = {
     ),
     "md_plan_destroy": (C.c_int, [_vp]),
     "md_plan_set_schedule": (C.c_int, [_vp, _i32]),
+    "md_plan_set_route": (C.c_int, [_vp, _i32, _i64]),
+    "md_last_route": (C.c_int, [_i32, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i32)]),
     "md_allreduce": (
         C.c_int,
         [_pp, _i32, _vp, _pp, _i64, _pp, _i32, _pp, _pp, _i64, _f32, _f32, _f32, _i64, _i32, _vp],
+    ),
+    "md_allreduce_ex": (
+        C.c_int, [_pp, _i32, _vp, _pp, _i64, _pp, _i32, C.POINTER(MdUpdate), _i64, _i32, _vp]
     ),
     "md_trace_dump": (C.c_int, [_i32, C.c_char_p]),
     "md_mix64": (_u64, [C.POINTER(_u64), _i32]),
@@ -145,3 +164,11 @@ def stream_ptr(stream) -> int | None:
     if stream is None:
         return None
     return int(stream.cuda_stream) or None
+
+
+def last_route(device: int) -> tuple[str, int, bool]:
+    """(route name, tile/segment elements, sharded) of the last md_allreduce
+    this process launched on ``device``."""
+    r, t, sh = C.c_int32(), C.c_int64(), C.c_int32()
+    check(load().md_last_route(int(device), C.byref(r), C.byref(t), C.byref(sh)))
+    return ROUTE_NAMES.get(r.value, str(r.value)), int(t.value), bool(sh.value)

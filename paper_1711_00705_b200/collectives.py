@@ -41,13 +41,14 @@ from paper_1711_00705_b200.topology import (
     star_fold_tables,
 )
 
-PIPELINE_DEPTH = 4             # reference constant (collectives.py:39); unused on device
 # Pipeline granularity (elements per flag), the reference's own default
 # (collectives.py:40). Bits do not depend on it; on B200 it is also the
 # measured optimum of the channelized kernel (64 KiB per source per segment;
 # sweep in profiles/README.md).
 DEFAULT_SEGMENT_ELEMS = 16384
 ALGORITHMS = ("multicolor", "ring", "reduce_bcast")
+# route of calls that leave ``route="auto"`` (tests pin every kernel through it)
+_DEFAULT_ROUTE = "auto"
 
 _MAX_SLICE = 1 << 31
 _SEG_BITS = 21      # the reference's tag layout bound, kept for make_segment_schedule
@@ -165,7 +166,15 @@ def elementwise_add(dst: GradientBuffer, src: GradientBuffer) -> None:
 @dataclass
 class SgdUpdate:
     """Fused SGD epilogue: W[:update_len] -= c * (g (+ wd_b*W)) with optional
-    momentum (include/mdb200.h, md_sgd_update)."""
+    momentum (include/mdb200.h, md_sgd_update).
+
+    ``sharded=True`` (md_allreduce_ex, MD_UPDATE_SHARDED): the owner of each
+    buffer slice updates it and pushes the new weights to every rank -- the
+    same weights bit for bit (replicas are identical, ref sgd.py:5-10) with
+    1/N of the update's HBM traffic per rank. Momentum becomes sharded state
+    (only this rank's slice is kept current) and the gradient buffer holds
+    the sum only on this rank's slice and past ``update_len``. The weights
+    are registered with every rank on first use (``ep.view_of``)."""
 
     weights: torch.Tensor
     c: float
@@ -173,6 +182,21 @@ class SgdUpdate:
     mu: float = 0.0
     wd_b: float = 0.0
     update_len: int | None = None
+    sharded: bool = False
+
+
+def _check_operand(ep, t, what: str) -> None:
+    """Device operands are passed by address: they must be float32, contiguous
+    and on the rank's device (a temporary contiguous copy would be freed
+    before the asynchronous kernel reads it)."""
+    if not (isinstance(t, torch.Tensor) and t.is_cuda):
+        raise InvalidConfig(f"{what} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise InvalidConfig(f"{what} must be float32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise InvalidConfig(f"{what} must be contiguous")
+    if t.device != ep.torch_device:
+        raise InvalidConfig(f"{what} on {t.device}, rank on {ep.torch_device}")
 
 
 def _device_tensor(ep, buf: GradientBuffer):
@@ -211,13 +235,17 @@ def run_fold(
     check: bool = True,
     ctas: int = 0,
     schedule: str = "tree",
+    route: str = "auto",
+    tile: int = 0,
 ) -> GradientBuffer:
     """One fused device collective: [worker fold] -> fold tree -> [SGD epilogue].
 
     ``schedule``: "tree" moves the data along each color's tree (the
     reference's schedule, collectives.py:225-296); "owner" cuts the buffer
     into n slices that one rank each folds with the same per-color fold order,
-    then broadcasts -- the same bits, balanced traffic for any k."""
+    then broadcasts -- the same bits, balanced traffic for any k.
+    ``route``/``tile``: pin the kernel (md_plan_set_route; "auto" picks by
+    size) -- every route gives the same bits."""
     if segment_elems < 1:
         raise InvalidConfig(f"segment_elems must be >= 1, got {segment_elems}")
     if schedule not in ("tree", "owner"):
@@ -228,24 +256,30 @@ def run_fold(
     n = dev.numel()
     wk = []
     for w in workers or []:
-        if not (isinstance(w, torch.Tensor) and w.is_cuda and w.dtype == torch.float32):
-            raise InvalidConfig("worker buffers must be float32 CUDA tensors")
+        _check_operand(ep, w, "worker buffer")
         if w.numel() != n:
             raise LengthMismatch(f"worker buffer of length {w.numel()} for payload {n}")
-        wk.append(w.contiguous().data_ptr())
+        wk.append(w.data_ptr())
     if len(wk) > _lib.MD_MAX_WORKERS:
         raise InvalidConfig(f"at most {_lib.MD_MAX_WORKERS} worker buffers")
     upd = None
     if update is not None:
         ulen = n if update.update_len is None else int(update.update_len)
-        if update.weights.numel() < ulen or update.weights.dtype != torch.float32:
+        _check_operand(ep, update.weights, "weights")
+        if update.weights.numel() < ulen:
             raise LengthMismatch("weights shorter than the update range")
         mom = update.momentum if (update.momentum is not None and update.mu != 0.0) else None
-        if mom is not None and mom.numel() < ulen:
-            raise LengthMismatch("momentum shorter than the update range")
-        upd = (update.weights.data_ptr(), mom.data_ptr() if mom is not None else None, ulen,
-               float(update.c), float(update.mu), float(update.wd_b))
-    plan = ep.plan(tables, schedule)
+        if mom is not None:
+            _check_operand(ep, mom, "momentum")
+            if mom.numel() < ulen:
+                raise LengthMismatch("momentum shorter than the update range")
+        sharded = bool(update.sharded) and ep.n_ranks > 1
+        # sharded: every rank's weights, as addressable from here
+        wptrs = ep.view_of(update.weights).ptrs if sharded else [update.weights.data_ptr()]
+        upd = (wptrs, mom.data_ptr() if mom is not None else None, ulen,
+               float(update.c), float(update.mu), float(update.wd_b),
+               _lib.MD_UPDATE_SHARDED if sharded else _lib.MD_UPDATE_REPLICATED)
+    plan = ep.plan(tables, schedule, _DEFAULT_ROUTE if route == "auto" else route, tile)
     arg = (ep.comm, view.ptrs, wk, upd)
     lib = _lib.load()
 
@@ -255,9 +289,13 @@ def run_fold(
         nw = len(args_list[0][2])
         wptrs = [p for a in args_list for p in a[2]]
         u0 = args_list[0][3]
-        ws = [a[3][0] for a in args_list] if u0 else []
-        ms = [a[3][1] for a in args_list] if u0 else []
-        rc = lib.md_allreduce(
+        u = None
+        if u0:
+            u = _lib.MdUpdate()
+            u.w = _lib.ptr_array([p for a in args_list for p in a[3][0]])
+            u.mom = _lib.ptr_array([a[3][1] for a in args_list]) if u0[1] else None
+            u.len, u.c, u.mu, u.wd_b, u.mode = u0[2], u0[3], u0[4], u0[5], u0[6]
+        rc = lib.md_allreduce_ex(
             _lib.ptr_array(comms),
             len(args_list),
             plan,
@@ -265,12 +303,7 @@ def run_fold(
             n,
             _lib.ptr_array(wptrs) if nw else None,
             nw,
-            _lib.ptr_array(ws) if u0 else None,
-            _lib.ptr_array(ms) if (u0 and u0[1]) else None,
-            u0[2] if u0 else 0,
-            u0[3] if u0 else 0.0,
-            u0[4] if u0 else 0.0,
-            u0[5] if u0 else 0.0,
+            C.byref(u) if u is not None else None,
             int(segment_elems),
             int(ctas),
             _lib.stream_ptr(ep.stream),
@@ -322,8 +355,7 @@ def allreduce_multicolor(
 ) -> GradientBuffer:
     """Sum buffers across ranks along k color trees (collectives.py:225-268)."""
     _debug_check_finite(buf)
-    if ep.n_ranks == 1 and not fused:
-        _ensure_length_agreement(ep, buf)
+    if ep.n_ranks == 1 and not fused:  # one rank always agrees with itself
         return buf
     if ep.n_ranks == 1:
         from paper_1711_00705_b200.topology import single_rank_tables
@@ -344,8 +376,7 @@ def allreduce_ring(
 ) -> GradientBuffer:
     """Reduce hop by hop to the ring root, broadcast back (collectives.py:302-359)."""
     _debug_check_finite(buf)
-    if ep.n_ranks == 1 and not fused:
-        _ensure_length_agreement(ep, buf)
+    if ep.n_ranks == 1 and not fused:  # one rank always agrees with itself
         return buf
     if ring is None:
         ring = build_ring(ep.n_ranks)
@@ -361,14 +392,9 @@ def reduce_then_broadcast(ep, buf: GradientBuffer, root: int = 0, **fused) -> Gr
     _debug_check_finite(buf)
     if not 0 <= root < ep.n_ranks:
         raise InvalidConfig(f"root {root} out of range")
-    if ep.n_ranks == 1 and not fused:
-        _ensure_length_agreement(ep, buf)
+    if ep.n_ranks == 1 and not fused:  # one rank always agrees with itself
         return buf
     return run_fold(ep, buf, star_fold_tables(ep.n_ranks, root), **fused)
-
-
-def _ensure_length_agreement(ep, buf: GradientBuffer) -> None:
-    return None  # a single rank always agrees with itself
 
 
 def allreduce(

@@ -34,6 +34,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "md_common.cuh"
@@ -50,6 +52,7 @@ constexpr int kUnroll = 2;
 
 struct Ctrl {
   unsigned long long arrive_len[MD_MAX_RANKS];  // from peer r: n | n_workers << 56
+  unsigned long long arrive_cfg[MD_MAX_RANKS];  // from peer r: its route word (cfg_word)
   uint32_t arrive_epoch[MD_MAX_RANKS];
   uint32_t done_epoch[MD_MAX_RANKS];
   uint32_t pad0[32 - 2 * MD_MAX_RANKS % 32];
@@ -116,6 +119,7 @@ struct ViewArgs {
   const float* workers[MD_MAX_WORKERS];
   float* w;
   float* mom;
+  float* peer_w[MD_MAX_RANKS];  // sharded update: every rank's weights (peer-mapped)
   int32_t* err;  // host-mapped: [code, detail]
   int32_t rank;
   uint32_t epoch;
@@ -139,11 +143,15 @@ struct AllreduceArgs {
   int32_t has_update, vec_ok;
   float c, mu, wd_b;
   struct TraceEv* trace;  // nullable: per-CTA event log (MD_AR_TRACE=1)
-  int32_t flag_gpu_fence;
-  int32_t reverse_local;   // local-only tasks walk their segments last-first  // publish with fence.acq_rel.gpu + relaxed sys stores
+  int32_t flag_gpu_fence;  // publish with fence.acq_rel.gpu + relaxed sys stores (publish_flags)
+  int32_t reverse_local;   // local-only tasks walk their segments last-first
   const FoldProg* prog;    // every color's fold program (one-shot / LL / stream / owner)
   int32_t prog_k;          // colors of the fold programs (the plan's k; a.k counts owner slices)
-  int32_t warp_fence;      // channel kernel: consumer warps fence their own stores (MD_AR_WARP_FENCE)
+  int32_t sharded;         // push kernel: sharded SGD update (W' pushed, momentum sharded)
+  // route word every rank publishes at the entry barrier: ranks that picked a
+  // different kernel / tile / segment / schedule / update mode fail together
+  // with InvalidConfig instead of exchanging differently-shaped flags
+  unsigned long long cfg_word;
   ViewArgs v[MD_MAX_RANKS];
 };
 
@@ -167,6 +175,8 @@ struct md_plan {
   std::vector<md::RankPlan> owner_host;  // owner-computes schedule (MD_SCHED_OWNER)
   md::RankPlan* owner_dev;
   int32_t schedule;                    // MD_SCHED_TREE / MD_SCHED_OWNER
+  int32_t route;                       // MD_ROUTE_* (md_plan_set_route; AUTO = by size)
+  int64_t tile;                        // tile override of the tiled routes (0 = auto)
 };
 
 namespace md {
@@ -627,6 +637,7 @@ __device__ bool entry_barrier(const AllreduceArgs& a, const ViewArgs& v, int loc
   if (local_cta == 0 && tid < a.n_ranks && tid != v.rank) {
     Ctrl* pc = v.peer_ctrl[tid];
     st_relaxed_sys64(reinterpret_cast<uint64_t*>(&pc->arrive_len[v.rank]), mylen);
+    st_relaxed_sys64(reinterpret_cast<uint64_t*>(&pc->arrive_cfg[v.rank]), a.cfg_word);
     __threadfence_system();
     st_release_sys(&pc->arrive_epoch[v.rank], epoch);
   }
@@ -644,6 +655,10 @@ __device__ bool entry_barrier(const AllreduceArgs& a, const ViewArgs& v, int loc
       if (len != mylen) {
         // every rank sees the same table, so every rank reports the mismatch
         if (local_cta == 0) raise_err(v, MD_ERR_LENGTH_MISMATCH, r);
+        ok = 0;
+      } else if (ld_relaxed_sys64(reinterpret_cast<const uint64_t*>(&v.ctrl->arrive_cfg[r])) !=
+                 a.cfg_word) {
+        if (local_cta == 0) raise_err(v, MD_ERR_INVALID_CONFIG, 8000 + r);
         ok = 0;
       }
     }
@@ -726,8 +741,6 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __shared__ __align__(8) uint64_t tma_full[kStages];
   extern __shared__ __align__(128) char ring[];  // kRingBytes of TMA stages
   uint32_t tma_seq = 0;                          // chunks through the ring so far
-  pdl_wait();  // the step's producer (gradient fill / fold inputs) has completed
-  pdl_launch_dependents();
   if (tid == 0) {
     s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
     for (int s = 0; s < kStages; ++s) mbar_init(&tma_full[s], 1);
@@ -1104,7 +1117,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
         s2 += m;
       }
       trace_ev(a, 2, cn, EV_DONE, pend[npend - 1]);
-      for (int i = 0; i < npend; ++i) publish_flags(a, v, t, pend[i], epoch, i == 0 && !a.warp_fence);
+      for (int i = 0; i < npend; ++i) publish_flags(a, v, t, pend[i], epoch, i == 0);
       trace_ev(a, 2, cn, EV_PUB, pend[npend - 1]);
       for (int i = 0; i < npend; ++i) {  // free the done slots for the consumers
         const uint32_t jj = j - npend + i;
@@ -1190,13 +1203,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
       if ((ct & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
     }
     // this warp is done with segment s: tell the notifier (the slot must have
-    // been acknowledged for the segment kDoneSlots earlier). warp_fence
-    // (opt-in MD_AR_WARP_FENCE=1): the warp makes its own stores GPU-visible
-    // here and the notifier publishes without a fence; measured slower (N = 2
-    // fused 100 MB: 194 -> 213 us -- each warp then waits for its W/momentum
-    // stores), neutral at N = 4
-    if (a.warp_fence && !((t.type != 0 || t.parent < 0) && t.n_down == 0))
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // been acknowledged for the segment kDoneSlots earlier)
     if ((ct & 31) == 0) {
       if (jseg >= kDoneSlots) {
         uint32_t spins = 0;
@@ -1231,7 +1238,6 @@ __global__ void __launch_bounds__(kArThreads, 1)
   if (a.prog)
     for (int i = tid; i < static_cast<int>(sizeof(FoldProg) / 4); i += blockDim.x)
       reinterpret_cast<uint32_t*>(&prog)[i] = reinterpret_cast<const uint32_t*>(a.prog)[i];
-  // prologue (SMEM only) overlaps the predecessor's drain under PDL
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -1248,8 +1254,6 @@ __global__ void __launch_bounds__(kArThreads, 1)
     s_idx = idx;
     s_m = m;
   }
-  pdl_wait();  // the step's producer (gradient fill / fold inputs) has completed
-  pdl_launch_dependents();
   if (tid == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
   __syncthreads();
   const uint32_t epoch = s_epoch;
@@ -1547,7 +1551,10 @@ __global__ void __launch_bounds__(kArThreads, 1)
     s_epoch = *reinterpret_cast<volatile uint32_t*>(&v.ctrl->epoch) + 1;
     for (int st = 0; st < S; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], kStreamConsumerWarps);
+      // the publisher counts in too: a stage is refilled only after its
+      // tile's read-done flags went out, so full[st] can never run a phase
+      // ahead of the publisher (parity aliasing -> cross-GPU deadlock)
+      mbar_init(&empty[st], kStreamConsumerWarps + 1);
       mbar_init(&clear[st], 1);
     }
     mbar_init_fence();
@@ -1600,6 +1607,7 @@ __global__ void __launch_bounds__(kArThreads, 1)
             if ((++spins & 1023) == 0 && aborted(v)) return;
           for (int r = 0; r < N; ++r)  // our reads of tile t completed (landed in SMEM)
             if (r != me) st_relaxed_sys(&v.peer_ctrl[r]->rd[me][t], epoch);
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[st])) : "memory");
         }
       }
     } else if (tid < kStreamConsumerBase) {  // ---------------- clearance ----------------
@@ -1715,18 +1723,23 @@ __global__ void __launch_bounds__(kArThreads, 1)
 // Owner-computes with a PUSHED broadcast: rank j pulls slice j of every rank
 // through a TMA ring, folds each element with its color program (same bits),
 // and TMA-bulk-stores the final tile into its own buffer AND every peer's --
-// no DOWN tasks, no per-segment flag fences. Slices are 16-byte aligned (the
-// <= 3 trailing elements of the buffer go to the last owner, scalar).
-// Plain calls: a peer needs the pushes only at the end of the call, which the
-// exit barrier's done flag certifies (each CTA waited for its bulk stores to
-// complete). Fused SGD calls (kEpi != 0): the owner updates W / momentum of
-// its own slice in the fold warps, and once a tile's bulk stores have
-// COMPLETED (cp.async.bulk.wait_group, no system fence: the flag follows the
-// finished writes) the storer sets a per-tile "landed" flag in every peer's
-// control block (rd[owner][tile]); a quarter of each rank's CTAs are
-// receivers that wait for those flags and apply the update to the pushed
-// tiles from local memory. Pulls and pushes split the 2 (N-1)/N bytes per
-// rank between the two protocols (measured ceilings ~650 / ~688 GB/s).
+// no DOWN tasks, no per-segment flags. Slices are 16-byte aligned (the <= 3
+// trailing elements of the buffer go to the last owner, scalar). A peer needs
+// the pushes only at the end of the call, which the exit barrier's done flag
+// certifies (each CTA waited for its bulk stores to complete). Pulls and
+// pushes split the 2 (N-1)/N bytes per rank between the two directions of
+// the links (measured ceilings ~650 / ~688 GB/s, profiles/README.md).
+//
+// Sharded SGD update (kEpi != 0; the host launches it only for
+// MD_UPDATE_SHARDED): replicas are bitwise equal (ref sgd.py:5-10), so the
+// owner of a slice may update it for everyone. The W and momentum rows of
+// the owner's slice arrive with the tile, the fold warps apply the update in
+// SMEM, and the storer pushes W' -- not g -- into every rank's weights, keeps
+// the momentum rows local (sharded optimizer state) and stores g into its own
+// buffer only. Buffer elements at or past update_len are pushed as in a
+// plain call. Same NVLink bytes as the plain call, 1/N of the update's HBM
+// traffic per rank, no per-tile signals (receivers need W' only at the end).
+// warp 0: TMA producer, warp 1: storer, warps 2..15: fold (+ update)
 constexpr int kPushConsumerBase = 64;
 constexpr int kPushConsumerWarps = kArThreads / 32 - 2;
 
@@ -1736,43 +1749,23 @@ __device__ __forceinline__ void bulk_store_nc(void* gdst, const void* ssrc, uint
                : "memory");
 }
 // 16-byte aligned slice j of an n-element buffer (the tail n & 3 is not in any)
-__device__ __forceinline__ void push_slice(int64_t n, int N, int j, int64_t* lo, int64_t* hi) {
+__host__ __device__ __forceinline__ void push_slice(int64_t n, int N, int j, int64_t* lo,
+                                                    int64_t* hi) {
   const int64_t n4 = n & ~int64_t(3);
   const int64_t per = ((n4 / 4 + N - 1) / N) * 4;
-  *lo = min(n4, static_cast<int64_t>(j) * per);
-  *hi = min(n4, static_cast<int64_t>(j + 1) * per);
-}
-// SGD update of [lo, hi) (16-byte aligned lo) from g in `g` (global, L1 bypass)
-template <int kEpi>
-__device__ __forceinline__ void push_epilogue(const AllreduceArgs& a, const ViewArgs& v,
-                                              int64_t lo, int64_t hi, int t0, int nt) {
-  constexpr bool kMom = kEpi >= 3;
-  const int64_t ulen4 = a.update_len & ~int64_t(3);
-  for (int64_t i = lo + 4 * t0; i < hi; i += 4 * static_cast<int64_t>(nt)) {
-    if (i + 4 <= ulen4) {
-      const float4 g = __ldcg(reinterpret_cast<const float4*>(v.buf + i));
-      float4 w = __ldcs(reinterpret_cast<const float4*>(v.w + i));
-      float4 m = kMom ? __ldcs(reinterpret_cast<const float4*>(v.mom + i))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-      sgd_elem<kEpi>(w.x, g.x, m.x, a);
-      sgd_elem<kEpi>(w.y, g.y, m.y, a);
-      sgd_elem<kEpi>(w.z, g.z, m.z, a);
-      sgd_elem<kEpi>(w.w, g.w, m.w, a);
-      __stcs(reinterpret_cast<float4*>(v.w + i), w);
-      if (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m);
-    } else {
-      for (int64_t q = i; q < min(hi, i + 4); ++q) epi_scalar<kEpi>(a, v, q, __ldcg(v.buf + q));
-    }
-  }
+  const int64_t l = static_cast<int64_t>(j) * per, h = static_cast<int64_t>(j + 1) * per;
+  *lo = l < n4 ? l : n4;
+  *hi = h < n4 ? h : n4;
 }
 
 template <int kEpi>
 __global__ void __launch_bounds__(kArThreads, 1)
     allreduce_push_kernel(const __grid_constant__ AllreduceArgs a) {
+  constexpr bool kUpd = kEpi != 0;
+  constexpr bool kMom = kEpi >= 3;
   const int view = blockIdx.x / a.ctas_per_view;
   const int local_cta = blockIdx.x % a.ctas_per_view;
-  const int G = a.max_stage;  // owner CTAs; local_cta >= G are receivers (fused only)
-  const int R = a.ctas_per_view - G;
+  const int G = a.ctas_per_view;
   const ViewArgs& v = a.v[view];
   const int tid = threadIdx.x;
   const int N = a.n_ranks, me = v.rank;
@@ -1781,8 +1774,11 @@ __global__ void __launch_bounds__(kArThreads, 1)
   int64_t A, B;
   push_slice(a.n, N, me, &A, &B);
   const int64_t T = (B - A + TE - 1) / TE;
+  const int64_t ulen = kUpd ? a.update_len : 0;  // a multiple of 4 (host)
   const size_t slot_f = static_cast<size_t>(TE);
-  const size_t stage_f = slot_f * (N + 1);  // [N rank slots][result]
+  const int w_slot = N + 1, m_slot = N + 2;
+  // [N rank slots][result g][W][momentum]
+  const size_t stage_f = slot_f * (N + 1 + (kUpd ? (kMom ? 2 : 1) : 0));
   __shared__ uint32_t s_epoch;
   __shared__ __align__(8) uint64_t full[8], empty[8], folded[8];
   __shared__ FoldProg prog;
@@ -1802,86 +1798,13 @@ __global__ void __launch_bounds__(kArThreads, 1)
   __syncthreads();
   const uint32_t epoch = s_epoch;
   const bool ok = entry_barrier(a, v, local_cta, epoch);
-  if (ok && local_cta >= G) [&]() {  // ---------------- receiver (fused only) ----------------
-    // batches of kRB tiles of the other slices (tile-major, so early tiles
-    // come first); every thread keeps 3 x kRB 16-byte loads in flight
-    constexpr int kRB = 4;
-    constexpr bool kMom = kEpi >= 3;
-    const int64_t ulen4 = a.update_len & ~int64_t(3);
-    int64_t l0, h0;
-    push_slice(a.n, N, 0, &l0, &h0);
-    const int64_t np = ((h0 - l0 + TE - 1) / TE) * (N - 1);  // (tile, source) pairs
-    __shared__ int64_t s_lo[kRB], s_hi[kRB];
-    for (int64_t p0 = static_cast<int64_t>(local_cta - G) * kRB; p0 < np; p0 += static_cast<int64_t>(R) * kRB) {
-      if (tid < kRB) {
-        s_lo[tid] = s_hi[tid] = 0;
-        const int64_t p = p0 + tid;
-        if (p < np) {
-          const int64_t t = p / (N - 1);
-          int r = static_cast<int>(p % (N - 1));
-          r += r >= me;
-          int64_t lo, hi;
-          push_slice(a.n, N, r, &lo, &hi);
-          if (lo + t * TE < hi) {
-            s_lo[tid] = lo + t * TE;
-            s_hi[tid] = min(hi, lo + t * TE + TE);
-            const uint32_t* f = &v.ctrl->rd[r][t];
-            if (!epoch_ge(ld_relaxed_sys(f), epoch)) {
-              const uint64_t t0 = globaltimer_ns();
-              uint32_t sp = 0;
-              while (!epoch_ge(ld_relaxed_sys(f), epoch)) {
-                if ((++sp & 1023) == 0) {
-                  if (aborted(v)) { s_hi[tid] = s_lo[tid]; break; }
-                  if (globaltimer_ns() - t0 > a.timeout_ns) {
-                    raise_err(v, MD_ERR_TIMEOUT, 7000 + r);
-                    s_hi[tid] = s_lo[tid];
-                    break;
-                  }
-                }
-              }
-            }
-          }
-        }
-      }
-      __syncthreads();
-      for (int64_t e = 4 * static_cast<int64_t>(tid); e < TE; e += 4 * static_cast<int64_t>(blockDim.x)) {
-        float4 g[kRB], w[kRB], m[kRB];
-        bool vec[kRB];
-#pragma unroll
-        for (int q = 0; q < kRB; ++q) {
-          const int64_t i = s_lo[q] + e;
-          vec[q] = i + 4 <= s_hi[q] && i + 4 <= ulen4;
-          if (vec[q]) {
-            g[q] = __ldcg(reinterpret_cast<const float4*>(v.buf + i));
-            w[q] = __ldcs(reinterpret_cast<const float4*>(v.w + i));
-            m[q] = kMom ? __ldcs(reinterpret_cast<const float4*>(v.mom + i))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < kRB; ++q) {
-          const int64_t i = s_lo[q] + e;
-          if (vec[q]) {
-            sgd_elem<kEpi>(w[q].x, g[q].x, m[q].x, a);
-            sgd_elem<kEpi>(w[q].y, g[q].y, m[q].y, a);
-            sgd_elem<kEpi>(w[q].z, g[q].z, m[q].z, a);
-            sgd_elem<kEpi>(w[q].w, g[q].w, m[q].w, a);
-            __stcs(reinterpret_cast<float4*>(v.w + i), w[q]);
-            if (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m[q]);
-          } else {
-            for (int64_t j = i; j < min(s_hi[q], i + 4); ++j) epi_scalar<kEpi>(a, v, j, __ldcg(v.buf + j));
-          }
-        }
-      }
-      __syncthreads();
-      if (aborted(v)) return;
-    }
-  }();
-  if (ok && local_cta < G) [&]() {
+  if (ok) [&]() {
     if (tid < 32) {  // ---------------- producer (+ the buffer's tail) ----------------
       if (tid != 0) return;
       if (me == N - 1 && local_cta == 0) {
-        for (int64_t i = a.n & ~int64_t(3); i < a.n; ++i) {  // <= 3 elements
+        // <= 3 elements past the last slice; update_len <= n & ~3 (host), so
+        // these are plain sums in every mode
+        for (int64_t i = a.n & ~int64_t(3); i < a.n; ++i) {
           float x[MD_MAX_RANKS];
           for (int r = 0; r < N; ++r) x[r] = r == me ? v.buf[i] : v.peer[r][i];
           const float g = fold_prog(prog.c[color_of(a.n, a.k, i)], x, 1, 0);
@@ -1900,20 +1823,20 @@ __global__ void __launch_bounds__(kArThreads, 1)
         }
         const int64_t lo = A + t * TE, hi = min(B, lo + TE);
         const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
+        const int64_t whi = min(hi, ulen);
+        const uint32_t wbytes = whi > lo ? static_cast<uint32_t>((whi - lo) * 4) : 0u;
         float* stage = ringf + st * stage_f;
-        mbar_expect_tx(&full[st], bytes * N);
+        mbar_expect_tx(&full[st], bytes * N + wbytes * (kMom ? 2 : 1));
         for (int r = 0; r < N; ++r)
           tma_load_1d(stage + r * slot_f, (r == me ? v.buf : v.peer[r]) + lo, bytes, &full[st]);
+        if (kUpd && wbytes) {
+          tma_load_1d(stage + w_slot * slot_f, v.w + lo, wbytes, &full[st]);
+          if (kMom) tma_load_1d(stage + m_slot * slot_f, v.mom + lo, wbytes, &full[st]);
+        }
       }
     } else if (tid < kPushConsumerBase) {  // ---------------- storer ----------------
       if (tid != 32) return;
       uint32_t seq = 0;
-      int64_t tprev = -1, tprev2 = -1;  // tiles whose writes may still be in flight
-      auto landed = [&](int64_t t) {  // per-tile flags for the receivers
-        if (kEpi == 0 || t < 0) return;
-        for (int r = 0; r < N; ++r)
-          if (r != me) st_relaxed_sys(&v.peer_ctrl[r]->rd[me][t], epoch);
-      };
       for (int64_t t = local_cta; t < T; t += G, ++seq) {
         const uint32_t st = seq % S;
         uint32_t spins = 0;
@@ -1921,10 +1844,31 @@ __global__ void __launch_bounds__(kArThreads, 1)
           if ((++spins & 1023) == 0 && aborted(v)) return;
         const int64_t lo = A + t * TE, hi = min(B, lo + TE);
         const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
-        const float* res = ringf + st * stage_f + N * slot_f;
-        for (int q = 0; q < N; ++q) {  // own buffer last: peers' pushes first on the wire
-          const int r = (me + 1 + q) % N;
-          bulk_store_nc((r == me ? v.buf : const_cast<float*>(v.peer[r])) + lo, res, bytes);
+        const float* stage = ringf + st * stage_f;
+        const float* res = stage + N * slot_f;
+        if (kUpd) {
+          const int64_t whi = min(hi, ulen);
+          if (whi > lo) {  // W' to every rank (own last: peers' pushes first on the wire)
+            const uint32_t wb = static_cast<uint32_t>((whi - lo) * 4);
+            for (int q = 0; q < N; ++q) {
+              const int r = (me + 1 + q) % N;
+              bulk_store_nc((r == me ? v.w : v.peer_w[r]) + lo, stage + w_slot * slot_f, wb);
+            }
+            if (kMom) bulk_store_nc(v.mom + lo, stage + m_slot * slot_f, wb);
+          }
+          const int64_t glo = max(lo, whi);
+          if (hi > glo)  // past the update range: g to every peer, as a plain call
+            for (int q = 0; q < N - 1; ++q) {
+              const int r = (me + 1 + q) % N;
+              bulk_store_nc(const_cast<float*>(v.peer[r]) + glo, res + (glo - lo),
+                            static_cast<uint32_t>((hi - glo) * 4));
+            }
+          bulk_store_nc(v.buf + lo, res, bytes);  // g: the own slice only
+        } else {
+          for (int q = 0; q < N; ++q) {  // own buffer last: peers' pushes first on the wire
+            const int r = (me + 1 + q) % N;
+            bulk_store_nc((r == me ? v.buf : const_cast<float*>(v.peer[r])) + lo, res, bytes);
+          }
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         if (seq >= 1) {  // the previous tile's stores have read their SMEM: free its stage
@@ -1932,17 +1876,9 @@ __global__ void __launch_bounds__(kArThreads, 1)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&empty[(seq - 1) % S]))
                        : "memory");
         }
-        if (kEpi != 0 && seq >= 2) {  // the tile before that has landed everywhere
-          asm volatile("cp.async.bulk.wait_group 2;" ::: "memory");
-          landed(tprev2);
-        }
-        tprev2 = tprev;
-        tprev = t;
       }
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every push has landed
-      landed(tprev2);
-      landed(tprev);
-    } else {  // ---------------- fold (+ own slice's SGD update) ----------------
+    } else {  // ---------------- fold (+ the slice's SGD update) ----------------
       const int ct = tid - kPushConsumerBase, nct = kPushConsumerWarps * 32;
       uint32_t seq = 0;
       for (int64_t t = local_cta; t < T; t += G, ++seq) {
@@ -1953,43 +1889,38 @@ __global__ void __launch_bounds__(kArThreads, 1)
         float* stage = ringf + st * stage_f;
         float* res = stage + N * slot_f;
         const int64_t lo = A + t * TE, len = min(B, lo + TE) - lo;
+        const int64_t wlen = kUpd ? max(int64_t(0), min(len, ulen - lo)) : 0;
         for (int64_t e = 4 * ct; e < len; e += 4 * nct) {
           const int c0 = color_of(a.n, a.k, lo + e);
+          float4 g;
           if (color_of(a.n, a.k, lo + e + 3) == c0) {
-            *reinterpret_cast<float4*>(res + e) = fold_prog4(prog.c[c0], stage, slot_f, e);
+            g = fold_prog4(prog.c[c0], stage, slot_f, e);
           } else {
-            for (int q = 0; q < 4; ++q)
-              res[e + q] = fold_prog(prog.c[color_of(a.n, a.k, lo + e + q)], stage, slot_f, e + q);
+            g.x = fold_prog(prog.c[c0], stage, slot_f, e);
+            g.y = fold_prog(prog.c[color_of(a.n, a.k, lo + e + 1)], stage, slot_f, e + 1);
+            g.z = fold_prog(prog.c[color_of(a.n, a.k, lo + e + 2)], stage, slot_f, e + 2);
+            g.w = fold_prog(prog.c[color_of(a.n, a.k, lo + e + 3)], stage, slot_f, e + 3);
+          }
+          *reinterpret_cast<float4*>(res + e) = g;
+          if constexpr (kUpd) {
+            if (e < wlen) {  // wlen is a multiple of 4
+              float4* wp = reinterpret_cast<float4*>(stage + w_slot * slot_f + e);
+              float4* mp = reinterpret_cast<float4*>(stage + m_slot * slot_f + e);
+              float4 w = *wp;
+              float4 m = kMom ? *mp : make_float4(0.f, 0.f, 0.f, 0.f);
+              sgd_elem<kEpi>(w.x, g.x, m.x, a);
+              sgd_elem<kEpi>(w.y, g.y, m.y, a);
+              sgd_elem<kEpi>(w.z, g.z, m.z, a);
+              sgd_elem<kEpi>(w.w, g.w, m.w, a);
+              *wp = w;
+              if (kMom) *mp = m;
+            }
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // SMEM -> bulk-store reads
         __syncwarp();
         if ((ct & 31) == 0)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&folded[st])) : "memory");
-        if constexpr (kEpi != 0) {  // own slice: W / momentum from the result in SMEM
-          constexpr bool kMom = kEpi >= 3;
-          const int64_t ulen4 = a.update_len & ~int64_t(3);
-          for (int64_t e = 4 * ct; e < len; e += 4 * nct) {
-            const int64_t i = lo + e;
-            const float4 g = *reinterpret_cast<const float4*>(res + e);
-            if (i + 4 <= ulen4) {
-              float4 w = __ldcs(reinterpret_cast<const float4*>(v.w + i));
-              float4 m = kMom ? __ldcs(reinterpret_cast<const float4*>(v.mom + i))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
-              sgd_elem<kEpi>(w.x, g.x, m.x, a);
-              sgd_elem<kEpi>(w.y, g.y, m.y, a);
-              sgd_elem<kEpi>(w.z, g.z, m.z, a);
-              sgd_elem<kEpi>(w.w, g.w, m.w, a);
-              __stcs(reinterpret_cast<float4*>(v.w + i), w);
-              if (kMom) __stcs(reinterpret_cast<float4*>(v.mom + i), m);
-            } else {
-              epi_scalar<kEpi>(a, v, i, g.x);
-              epi_scalar<kEpi>(a, v, i + 1, g.y);
-              epi_scalar<kEpi>(a, v, i + 2, g.z);
-              epi_scalar<kEpi>(a, v, i + 3, g.w);
-            }
-          }
-        }
       }
     }
   }();
@@ -2377,6 +2308,8 @@ int md_plan_create(int32_t n_ranks, int32_t k, const int32_t* parent, const int3
   p->prog_dev = nullptr;
   p->owner_dev = nullptr;
   p->schedule = MD_SCHED_TREE;
+  p->route = MD_ROUTE_AUTO;
+  p->tile = 0;
   FoldProg prog;
   build_fold_prog(host, n_ranks, k, &prog);
   build_owner_plans(n_ranks, &p->owner_host);
@@ -2408,6 +2341,16 @@ int md_plan_set_schedule(md_plan_t* p, int32_t schedule) {
   return MD_OK;
 }
 
+int md_plan_set_route(md_plan_t* p, int32_t route, int64_t tile) {
+  if (!p || route < MD_ROUTE_AUTO || route > MD_ROUTE_PUSH || tile < 0) {
+    set_error("bad plan, route %d or tile %lld", route, (long long)tile);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  p->route = route;
+  p->tile = tile & ~int64_t(3);
+  return MD_OK;
+}
+
 int md_plan_destroy(md_plan_t* p) {
   if (!p) return MD_OK;
   int prev;
@@ -2421,23 +2364,55 @@ int md_plan_destroy(md_plan_t* p) {
   return MD_OK;
 }
 
+}  // extern "C"
+
+namespace {
+using namespace md;
+
+// Routing knobs, read ONCE per process (the environment is for tools and A/B
+// runs; tests and callers pick routes per plan with md_plan_set_route).
+struct ArEnv {
+  int64_t ll_max = -1;       // MD_AR_LL_MAX: largest LL buffer (bytes), -1 = built-in
+  int64_t oneshot_max = -1;  // MD_AR_ONESHOT_MAX
+  int32_t route = MD_ROUTE_AUTO;  // MD_AR_ROUTE=tree|queue|ll|oneshot|stream|push
+  int64_t tile = 0;          // MD_AR_TILE: tile of the tiled routes (elements)
+  int32_t lag = -1;          // MD_AR_LAG: queue kernel pipeline lag
+  bool trace = false;        // MD_AR_TRACE=1: per-CTA event log (md_trace_dump)
+  bool sys_fence = false;    // MD_AR_SYS_FENCE=1: system-scope release for every flag
+};
+
+const ArEnv& ar_env() {
+  static const ArEnv env = [] {
+    ArEnv e;
+    if (const char* x = getenv("MD_AR_LL_MAX")) e.ll_max = atoll(x);
+    if (const char* x = getenv("MD_AR_ONESHOT_MAX")) e.oneshot_max = atoll(x);
+    if (const char* x = getenv("MD_AR_TILE")) e.tile = std::max<int64_t>(0, atoll(x)) & ~int64_t(3);
+    if (const char* x = getenv("MD_AR_LAG")) e.lag = std::max(0, atoi(x));
+    e.trace = getenv("MD_AR_TRACE") != nullptr;
+    e.sys_fence = getenv("MD_AR_SYS_FENCE") != nullptr;
+    if (const char* x = getenv("MD_AR_ROUTE")) {
+      static const char* names[] = {"auto", "tree", "queue", "ll", "oneshot", "stream", "push"};
+      for (int r = 0; r <= MD_ROUTE_PUSH; ++r)
+        if (!strcmp(x, names[r])) e.route = r;
+    }
+    return e;
+  }();
+  return env;
+}
+
 // Smallest plain buffer (bytes) the owner-push kernel takes by default.
 // Measured against the tree (graph-timed sweep, profiles/README.md): N = 2
 // faster from 64 MiB (117 vs 127 us; 1 GiB 662 vs 645 GB/s bus) but slower at
 // 16 MiB; N = 4 faster from 4 MiB (31.6 vs 34.6 us) to 1 GiB (622 vs 601),
 // within 2 % at 256 MiB.
-static int64_t push_min_bytes(int N) {
-  return N == 2 ? (int64_t(32) << 20) : (int64_t(2) << 20);
-}
+int64_t push_min_bytes(int N) { return N == 2 ? (int64_t(32) << 20) : (int64_t(2) << 20); }
 
 // Pipeline segment cap for a color chunk of `chunk` elements: about two
 // segments per SM, never below 4096 elements (the per-segment flag cost).
 // segment_elems is an upper bound only -- the bits never depend on it
 // (pkg/tests/test_collectives.py:131-147). Measured at N = 4, k = 4: 4 MiB
 // 38.3 -> 35.3 us, 16 MiB 65.9 -> 62 us; 100 MB unchanged (16384 stays).
-static int64_t auto_seg(int64_t chunk) {
-  int dev = 0;
-  cudaGetDevice(&dev);
+int64_t auto_seg(int64_t chunk, int dev) {
   const int64_t want = (chunk / (2 * static_cast<int64_t>(sm_count(dev))) + 3) & ~int64_t(3);
   return std::max<int64_t>(4096, want);
 }
@@ -2445,36 +2420,121 @@ static int64_t auto_seg(int64_t chunk) {
 // Largest buffer (bytes) the one-shot kernel takes at world size N: at N = 2
 // its ingress equals the tree's, so any size that fits; above, it pulls
 // (N-1) x bytes against the tree's 2 (N-1)/N x bytes, so only latency-bound
-// sizes (measured crossover, profiles/README.md). MD_AR_ONESHOT_MAX overrides
-// (0 disables the path).
-static int64_t oneshot_max_bytes(int N) {
-  if (const char* e = getenv("MD_AR_ONESHOT_MAX")) return atoll(e);
+// sizes (measured crossover, profiles/README.md).
+int64_t oneshot_max_bytes(int N) {
+  if (ar_env().oneshot_max >= 0) return ar_env().oneshot_max;
   return N == 2 ? (int64_t(1) << 40) : (int64_t(1) << 20);
 }
 
-// Smallest buffer (bytes) a fused N = 2 call streams (measured win at the
-// 102.4 MB C5 buffer; below that the tree keeps it). MD_AR_STREAM overrides.
-static int64_t stream_min_bytes() { return int64_t(64) << 20; }
+// Smallest buffer (bytes) a replicated fused N = 2 call streams (measured win
+// at the 102.4 MB C5 buffer; below that the tree keeps it).
+constexpr int64_t kStreamMinBytes = int64_t(64) << 20;
 
 // Largest buffer (bytes) the LL push kernel takes: it moves 2 x (N-1) x bytes
 // out of every rank (value + epoch words), so only latency-bound sizes:
 // measured faster than the one-shot pull up to 1 MiB at N = 2 and 4 (10.4 vs
 // 15.9 us and 20.0 vs 21.3 us), untested above N = 4 (256 KiB there).
-// MD_AR_LL_MAX overrides (0 disables the path).
-static int64_t ll_max_bytes(int N) {
-  if (const char* e = getenv("MD_AR_LL_MAX")) return atoll(e);
+int64_t ll_max_bytes(int N) {
+  if (ar_env().ll_max >= 0) return ar_env().ll_max;
   return N <= 4 ? (int64_t(1) << 20) : (int64_t(256) << 10);
+}
+
+// cudaFuncSetAttribute(max dynamic SMEM) once per (kernel, device)
+int smem_attr_once(const void* k, int dev, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> g(mu);
+  for (const auto& d : done)
+    if (d.first == k && d.second == dev) return MD_OK;
+  MD_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(bytes)));
+  done.emplace_back(k, dev);
+  return MD_OK;
+}
+
+// Emulated ranks (n_views > 1) wait on each other's CTAs on ONE device: a
+// cooperative launch guarantees they are co-resident. A real rank's CTAs only
+// wait on other GPUs (never on a sibling CTA), so a plain launch of <= one
+// CTA per SM is deadlock-free there.
+int launch_views(const void* k, unsigned grid, int n_views, size_t smem, AllreduceArgs* a,
+                 void* stream) {
+  void* args[] = {a};
+  if (n_views > 1) {
+    MD_CUDA_TRY(cudaLaunchCooperativeKernel(k, dim3(grid * n_views), dim3(kArThreads), args, smem,
+                                            as_stream(stream)));
+  } else {
+    MD_CUDA_TRY(cudaLaunchKernel(k, dim3(grid), dim3(kArThreads), args, smem, as_stream(stream)));
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return MD_OK;
+}
+
+#define MD_EPI_TABLE(kernel)                                                                   \
+  static const void* kernel##_of(int epi) {                                                    \
+    switch (epi) {                                                                             \
+      case 1: return reinterpret_cast<const void*>(kernel<1>);                                 \
+      case 2: return reinterpret_cast<const void*>(kernel<2>);                                 \
+      case 3: return reinterpret_cast<const void*>(kernel<3>);                                 \
+      case 4: return reinterpret_cast<const void*>(kernel<4>);                                 \
+      default: return reinterpret_cast<const void*>(kernel<0>);                                \
+    }                                                                                          \
+  }
+MD_EPI_TABLE(allreduce_ll_kernel)
+MD_EPI_TABLE(allreduce_oneshot_kernel)
+MD_EPI_TABLE(allreduce_stream_kernel)
+MD_EPI_TABLE(allreduce_push_kernel)
+MD_EPI_TABLE(allreduce_channels_kernel)
+MD_EPI_TABLE(allreduce_kernel)
+#undef MD_EPI_TABLE
+
+std::atomic<uint64_t> g_last_route[64];
+
+void record_route(int dev, int route, int64_t tile, bool sharded) {
+  if (dev >= 0 && dev < 64)
+    g_last_route[dev].store(static_cast<uint64_t>(route) | (sharded ? 0x80u : 0u) |
+                                (static_cast<uint64_t>(tile) << 8),
+                            std::memory_order_relaxed);
+}
+
+uint64_t cfg_word_of(int route, bool owner_sched, bool sharded, int64_t geometry) {
+  return static_cast<uint64_t>(route) | (static_cast<uint64_t>(owner_sched) << 4) |
+         (static_cast<uint64_t>(sharded) << 5) | (static_cast<uint64_t>(geometry) << 8);
+}
+
+}  // namespace
+
+extern "C" {
+
+int md_last_route(int32_t device, int32_t* route, int64_t* tile, int32_t* sharded) {
+  if (device < 0 || device >= 64) {
+    set_error("bad device %d", device);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  const uint64_t w = g_last_route[device].load(std::memory_order_relaxed);
+  if (route) *route = static_cast<int32_t>(w & 0x7f);
+  if (sharded) *sharded = (w & 0x80) ? 1 : 0;
+  if (tile) *tile = static_cast<int64_t>(w >> 8);
+  return MD_OK;
 }
 
 int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan,
                  float* const* bufs, int64_t n, const float* const* workers, int32_t n_workers,
                  float* const* w, float* const* mom, int64_t update_len, float c, float mu,
                  float wd_b, int64_t seg_elems, int32_t ctas, void* stream) {
+  md_update_t u{w, mom, update_len, c, mu, wd_b, MD_UPDATE_REPLICATED};
+  return md_allreduce_ex(comms, n_views, plan, bufs, n, workers, n_workers, w ? &u : nullptr,
+                         seg_elems, ctas, stream);
+}
+
+int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan,
+                    float* const* bufs, int64_t n, const float* const* workers, int32_t n_workers,
+                    const md_update_t* upd, int64_t seg_elems, int32_t ctas, void* stream) {
   if (!plan || n_views < 1 || n_views > MD_MAX_RANKS) {
     set_error("bad plan/view count");
     return MD_ERR_INVALID_CONFIG;
   }
   const int N = plan->n_ranks;
+  const ArEnv& env = ar_env();
   if (n < 0) {
     set_error("negative length");
     return MD_ERR_INVALID_CONFIG;
@@ -2487,11 +2547,21 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     set_error("segment_elems must be >= 1, got %lld", (long long)seg_elems);
     return MD_ERR_INVALID_CONFIG;
   }
-  const bool has_update = w != nullptr;
+  const bool has_update = upd != nullptr && upd->w != nullptr;
+  const int64_t update_len = has_update ? upd->len : 0;
   if (has_update && (update_len < 0 || update_len > n)) {
     set_error("update_len %lld outside [0, %lld]", (long long)update_len, (long long)n);
     return MD_ERR_LENGTH_MISMATCH;
   }
+  if (has_update && upd->mode != MD_UPDATE_REPLICATED && upd->mode != MD_UPDATE_SHARDED) {
+    set_error("bad update mode %d", upd->mode);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  const bool mode_sharded = has_update && upd->mode == MD_UPDATE_SHARDED;
+  const float c = has_update ? upd->c : 0.f, mu = has_update ? upd->mu : 0.f;
+  const float wd_b = has_update ? upd->wd_b : 0.f;
+  int dev;
+  MD_CUDA_TRY(cudaGetDevice(&dev));
   AllreduceArgs a;
   memset(&a, 0, sizeof(a));
   a.plan = plan->dev;
@@ -2501,22 +2571,20 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   a.n_views = n_views;
   a.n_workers = n_workers;
   a.has_update = has_update;
-  a.update_len = has_update ? update_len : 0;
+  a.update_len = update_len;
   a.c = c;
   a.mu = mu;
   a.wd_b = wd_b;
+  a.flag_gpu_fence = !env.sys_fence;  // see publish_flags
+  a.reverse_local = 1;
+  a.prog = plan->prog_dev;
+  a.prog_k = plan->k;
   // segment length: multiple of 4 elements, <= kMaxSegs segments per color
-  int64_t maxlen = (n + plan->k - 1) / plan->k;
+  const int64_t maxlen = (n + plan->k - 1) / plan->k;
   int64_t seg = std::max<int64_t>(4, (seg_elems + 3) & ~int64_t(3));
-  if (N > 1) seg = std::min(seg, auto_seg(maxlen));
-  int64_t min_seg = ((maxlen + 3) / kMaxSegs + 4 + 3) & ~int64_t(3);
+  if (N > 1) seg = std::min(seg, auto_seg(maxlen, dev));
+  const int64_t min_seg = ((maxlen + 3) / kMaxSegs + 4 + 3) & ~int64_t(3);
   if (seg < min_seg) seg = min_seg;
-  if (N == 1) {
-    // nothing to pipeline against: ~2 items per SM amortise the per-item
-    // queue/flag overhead of the streaming SGD epilogue
-    int64_t big = ((maxlen / (2 * sm_count(0)) + 1023) / 1024) * 1024;
-    seg = std::max(seg, big);
-  }
   a.seg = seg;
   int64_t mx = 0;
   for (int col = 0; col < plan->k; ++col) {
@@ -2551,8 +2619,14 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
       bits |= reinterpret_cast<uintptr_t>(v.workers[j]);
     }
     if (has_update) {
-      v.w = w[vi];
-      v.mom = (mom && mu != 0.f) ? mom[vi] : nullptr;
+      // sharded: w holds every rank's (peer-mapped) weights, view-major
+      v.w = mode_sharded ? upd->w[vi * N + cm->rank] : upd->w[vi];
+      if (mode_sharded)
+        for (int r = 0; r < N; ++r) {
+          v.peer_w[r] = upd->w[vi * N + r];
+          bits |= reinterpret_cast<uintptr_t>(v.peer_w[r]);
+        }
+      v.mom = (upd->mom && mu != 0.f) ? upd->mom[vi] : nullptr;
       bits |= reinterpret_cast<uintptr_t>(v.w) | reinterpret_cast<uintptr_t>(v.mom);
     }
     v.err = cm->err_dev;
@@ -2561,234 +2635,142 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
   }
   a.vec_ok = (bits & 15) == 0;
   a.timeout_ns = static_cast<unsigned long long>(timeout * 1e9);
+  const int req = plan->route != MD_ROUTE_AUTO ? plan->route : env.route;
+  const int64_t tile_req = plan->tile ? plan->tile : env.tile;
+  const bool auto_route = req == MD_ROUTE_AUTO;
+  const int avail = sm_count(dev) / n_views;  // CTAs (one per SM) per view
+  const bool fold_ok = N > 1 && n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev;
 
   // One rank, no worker fold: the collective is the identity and the call is
   // only its fused SGD update -- the streaming md_sgd_update kernel (8 CTAs x
   // 256 threads per SM) measured 82 vs 91 us for the 25.6M-float momentum +
   // weight-decay update (95 % vs 86 % of the HBM copy peak); same sgd1 math.
-  if (N == 1 && n_views == 1 && n_workers == 0 && !getenv("MD_AR_N1_FUSED")) {
+  if (N == 1 && n_views == 1 && n_workers == 0) {
+    record_route(dev, MD_ROUTE_LOCAL, 0, false);
     if (!has_update || update_len == 0) return MD_OK;
     return md_sgd_update(a.v[0].w, a.v[0].buf, a.v[0].mom, update_len, c,
                          a.v[0].mom ? mu : 0.f, wd_b, stream);
   }
-
-  int dev;
-  MD_CUDA_TRY(cudaGetDevice(&dev));
-  int per_sm = 0;
   int epi = 0;
   if (has_update) epi = (a.v[0].mom ? 3 : 1) + (wd_b != 0.f ? 1 : 0);
 
-  // LL (push) path for the smallest buffers: see allreduce_ll_kernel.
-  const int ll_avail = sm_count(dev) / n_views;
-  const int64_t ll_g = std::min<int64_t>(ll_avail, std::max<int64_t>(1, (n + 255) / 256));
-  const int64_t ll_e = ll_g > 0 ? (((n + ll_g - 1) / ll_g) + 3) & ~int64_t(3) : 0;
-  if (N > 1 && n > 0 && n <= kLLElems && n_workers == 0 && a.vec_ok && plan->prog_dev &&
-      n * 4 <= ll_max_bytes(N) && ll_avail >= 1 && N * ll_e * 4 <= int64_t(kRingBytes)) {
-    const int64_t E = ll_e;
-    const int64_t g = (n + E - 1) / E;
-    a.seg = E;
-    a.ctas_per_view = static_cast<int32_t>(g);
-    a.prog = plan->prog_dev;
-    const void* lk = nullptr;
-    switch (epi) {
-      case 1: lk = (const void*)allreduce_ll_kernel<1>; break;
-      case 2: lk = (const void*)allreduce_ll_kernel<2>; break;
-      case 3: lk = (const void*)allreduce_ll_kernel<3>; break;
-      case 4: lk = (const void*)allreduce_ll_kernel<4>; break;
-      default: lk = (const void*)allreduce_ll_kernel<0>; break;
+  // ---- owner-push: plain buffers from push_min_bytes(N), and every sharded
+  // update (W' pushed, momentum sharded; see allreduce_push_kernel)
+  {
+    const bool shard_ok = mode_sharded && (update_len & 3) == 0;
+    const bool want = shard_ok ? (auto_route || req == MD_ROUTE_PUSH)
+                               : epi == 0 && (req == MD_ROUTE_PUSH ||
+                                              (auto_route && n * 4 >= push_min_bytes(N)));
+    if (want && fold_ok && avail >= 1) {
+      // tile: deep enough rings for the N sources (measured, graph-timed 1 GiB:
+      // N = 4 2048 -> 2361 us vs 4096 -> 2596 us; N = 2 3072 -> 1615 vs 1636)
+      int64_t TE = tile_req ? tile_req : (N == 2 ? 3072 : 2048);
+      int64_t A0, B0;
+      push_slice(n, N, 0, &A0, &B0);
+      while ((B0 - A0 + TE - 1) / TE > kMaxTiles) TE *= 2;
+      const int ups = epi == 0 ? 0 : (epi >= 3 ? 2 : 1);
+      const int64_t stage_bytes = static_cast<int64_t>(N + 1 + ups) * TE * 4;
+      const int S = static_cast<int>(std::min<int64_t>(8, kStreamRingBytes / stage_bytes));
+      if (S >= 2) {
+        const int64_t T = std::max<int64_t>(1, (B0 - A0 + TE - 1) / TE);
+        const int g = static_cast<int>(std::min<int64_t>(avail, T));
+        a.seg = TE;
+        a.lag = S;
+        a.ctas_per_view = g;
+        a.sharded = shard_ok;
+        a.cfg_word = cfg_word_of(MD_ROUTE_PUSH, false, shard_ok, TE);
+        const void* k = allreduce_push_kernel_of(epi);
+        const size_t smem = static_cast<size_t>(S) * stage_bytes;
+        int rc = smem_attr_once(k, dev, kStreamRingBytes);
+        if (rc == MD_OK) rc = launch_views(k, g, n_views, smem, &a, stream);
+        if (rc == MD_OK) record_route(dev, MD_ROUTE_PUSH, TE, shard_ok);
+        return rc;
+      }
     }
-    const size_t smem = static_cast<size_t>(N) * E * 4;
-    static std::atomic<uint32_t> ll_set[64];
-    const uint32_t lbit = 1u << epi;
-    if (dev < 0 || dev >= 64 || !(ll_set[dev].load() & lbit)) {
-      MD_CUDA_TRY(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kRingBytes)));
-      if (dev >= 0 && dev < 64) ll_set[dev].fetch_or(lbit);
-    }
-    void* args[] = {&a};
-    if (n_views > 1 || getenv("MD_AR_COOP")) {
-      MD_CUDA_TRY(cudaLaunchCooperativeKernel(lk, dim3(static_cast<unsigned>(g) * n_views),
-                                              dim3(kArThreads), args, smem, as_stream(stream)));
-    } else {
-      MD_CUDA_TRY(cudaLaunchKernel(lk, dim3(static_cast<unsigned>(g)), dim3(kArThreads), args,
-                                   smem, as_stream(stream)));
-    }
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return MD_OK;
   }
 
-  // one-shot (latency) path for buffers that fit one SMEM pass of every rank's
-  // data: see allreduce_oneshot_kernel. Same bits as the tree schedule.
-  if (N > 1 && n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
+  // ---- LL push (the smallest buffers): see allreduce_ll_kernel
+  {
+    const int64_t g0 = std::min<int64_t>(avail, std::max<int64_t>(1, (n + 255) / 256));
+    const int64_t E = g0 > 0 ? (((n + g0 - 1) / g0) + 3) & ~int64_t(3) : 0;
+    const bool want = req == MD_ROUTE_LL || (auto_route && n * 4 <= ll_max_bytes(N));
+    if (want && fold_ok && n <= kLLElems && avail >= 1 && N * E * 4 <= int64_t(kRingBytes)) {
+      const int64_t g = (n + E - 1) / E;
+      a.seg = E;
+      a.ctas_per_view = static_cast<int32_t>(g);
+      const void* k = allreduce_ll_kernel_of(epi);
+      int rc = smem_attr_once(k, dev, kRingBytes);
+      if (rc == MD_OK)
+        rc = launch_views(k, static_cast<unsigned>(g), n_views, static_cast<size_t>(N) * E * 4,
+                          &a, stream);
+      if (rc == MD_OK) record_route(dev, MD_ROUTE_LL, E, false);
+      return rc;
+    }
+  }
+
+  // ---- one-shot pull (buffers that fit one SMEM pass of every rank's data)
+  {
     const int64_t emax = static_cast<int64_t>(kRingBytes / 4u / N) & ~int64_t(3);
-    const int avail = sm_count(dev) / n_views;
     int64_t g = std::min<int64_t>(avail, std::max<int64_t>(1, (n + 1023) / 1024));
     const int64_t E = (((n + g - 1) / g) + 3) & ~int64_t(3);
-    if (E <= emax && n * 4 <= oneshot_max_bytes(N) && avail >= 1) {
+    const bool want = req == MD_ROUTE_ONESHOT || (auto_route && n * 4 <= oneshot_max_bytes(N));
+    if (want && fold_ok && avail >= 1 && E <= emax) {
       g = (n + E - 1) / E;
       a.seg = E;
       a.ctas_per_view = static_cast<int32_t>(g);
-      a.prog = plan->prog_dev;
-      const void* ok = nullptr;
-      switch (epi) {
-        case 1: ok = (const void*)allreduce_oneshot_kernel<1>; break;
-        case 2: ok = (const void*)allreduce_oneshot_kernel<2>; break;
-        case 3: ok = (const void*)allreduce_oneshot_kernel<3>; break;
-        case 4: ok = (const void*)allreduce_oneshot_kernel<4>; break;
-        default: ok = (const void*)allreduce_oneshot_kernel<0>; break;
-      }
-      static std::atomic<uint32_t> os_set[64];
-      const uint32_t obit = 1u << epi;
-      if (dev < 0 || dev >= 64 || !(os_set[dev].load() & obit)) {
-        MD_CUDA_TRY(cudaFuncSetAttribute(ok, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kRingBytes)));
-        if (dev >= 0 && dev < 64) os_set[dev].fetch_or(obit);
-      }
-      const size_t smem = static_cast<size_t>(N) * E * 4;
-      void* args[] = {&a};
-      if (n_views > 1 || getenv("MD_AR_COOP")) {
-        MD_CUDA_TRY(cudaLaunchCooperativeKernel(ok, dim3(static_cast<unsigned>(g) * n_views),
-                                                dim3(kArThreads), args, smem, as_stream(stream)));
-      } else {
-        cudaLaunchConfig_t cfg{};
-        cudaLaunchAttribute at[1];
-        pdl_config(&cfg, at, dim3(static_cast<unsigned>(g)), dim3(kArThreads), smem,
-                   as_stream(stream));
-        MD_CUDA_TRY(cudaLaunchKernelExC(&cfg, ok, args));
-      }
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      return MD_OK;
+      a.cfg_word = cfg_word_of(MD_ROUTE_ONESHOT, false, false, E);
+      const void* k = allreduce_oneshot_kernel_of(epi);
+      int rc = smem_attr_once(k, dev, kRingBytes);
+      if (rc == MD_OK)
+        rc = launch_views(k, static_cast<unsigned>(g), n_views, static_cast<size_t>(N) * E * 4,
+                          &a, stream);
+      if (rc == MD_OK) record_route(dev, MD_ROUTE_ONESHOT, E, false);
+      return rc;
     }
   }
-  const void* kern = nullptr;
-  // stream (all-pull, tiled) kernel: see allreduce_stream_kernel. Default for
-  // FUSED calls at N = 2 from stream_min_bytes() up, with balanced tiles of
-  // <= 6656 floats (two stages of [2 ranks | W | momentum] in the 224 KB
-  // ring): C5 step at N = 2, graph-timed, 206 -> 198 us (allreduce 197 -> 189
-  // us; tiles 5120 / 6144 / 7168 measured 210 / 189-193 / 193 us,
-  // profiles/README.md). At N > 2 it pulls (N-1) x bytes and loses (N = 4:
-  // 502 vs 275 us), so there it is opt-in only. MD_AR_STREAM=0/1 overrides
-  // the choice, MD_AR_TILE the tile.
+
+  // ---- stream (all-pull, tiled): replicated fused calls at N = 2 from 64 MiB,
+  // balanced tiles of <= 6656 floats (two stages of [2 ranks | W | momentum]
+  // in the 224 KB ring): C5 step at N = 2, graph-timed, 206 -> 198 us
+  // (profiles/README.md). At N > 2 it pulls (N-1) x bytes and loses (N = 4:
+  // 502 vs 275 us), so there it only runs when asked for.
   {
-    const char* se = getenv("MD_AR_STREAM");
-    const bool want = se ? atoi(se) != 0 : (N == 2 && epi != 0 && n * 4 >= stream_min_bytes());
-    if (want && N > 1 && n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
+    const bool want =
+        req == MD_ROUTE_STREAM || (auto_route && N == 2 && epi != 0 && n * 4 >= kStreamMinBytes);
+    if (want && fold_ok && avail >= 1) {
       int64_t TE = 2048;
       if (N == 2) {  // balanced: every CTA gets the same number of tiles
-        const int64_t G = std::max(1, sm_count(dev) / n_views);
-        const int64_t rounds = std::max<int64_t>(1, (n + G * 6656 - 1) / (G * 6656));
-        TE = std::max<int64_t>(4, ((n + G * rounds - 1) / (G * rounds) + 3) & ~int64_t(3));
+        const int64_t rounds = std::max<int64_t>(1, (n + avail * 6656 - 1) / (avail * 6656));
+        TE = std::max<int64_t>(4, ((n + avail * rounds - 1) / (avail * rounds) + 3) & ~int64_t(3));
       }
-      if (const char* te = getenv("MD_AR_TILE")) TE = std::max<int64_t>(4, atoll(te) & ~int64_t(3));
+      if (tile_req) TE = tile_req;
       while ((n + TE - 1) / TE > kMaxTiles) TE *= 2;
       const int epi_slots = epi == 0 ? 0 : (epi >= 3 ? 2 : 1);
       const int64_t stage_bytes = static_cast<int64_t>(N + epi_slots) * TE * 4;
       const int S = static_cast<int>(std::min<int64_t>(8, kStreamRingBytes / stage_bytes));
-      const int avail = sm_count(dev) / n_views;
-      if (S >= 2 && avail >= 1) {
+      if (S >= 2) {
         const int64_t T = (n + TE - 1) / TE;
         const int g = static_cast<int>(std::min<int64_t>(avail, T));
         a.seg = TE;
         a.lag = S;
         a.ctas_per_view = g;
-        a.prog = plan->prog_dev;
-        const void* sk = nullptr;
-        switch (epi) {
-          case 1: sk = (const void*)allreduce_stream_kernel<1>; break;
-          case 2: sk = (const void*)allreduce_stream_kernel<2>; break;
-          case 3: sk = (const void*)allreduce_stream_kernel<3>; break;
-          case 4: sk = (const void*)allreduce_stream_kernel<4>; break;
-          default: sk = (const void*)allreduce_stream_kernel<0>; break;
-        }
-        static std::atomic<uint32_t> st_set[64];
-        const uint32_t sbit = 1u << epi;
-        if (dev < 0 || dev >= 64 || !(st_set[dev].load() & sbit)) {
-          MD_CUDA_TRY(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kStreamRingBytes)));
-          if (dev >= 0 && dev < 64) st_set[dev].fetch_or(sbit);
-        }
-        const size_t smem = static_cast<size_t>(S) * stage_bytes;
-        void* args[] = {&a};
-        if (n_views > 1 || getenv("MD_AR_COOP")) {
-          MD_CUDA_TRY(cudaLaunchCooperativeKernel(sk, dim3(static_cast<unsigned>(g) * n_views),
-                                                  dim3(kArThreads), args, smem,
-                                                  as_stream(stream)));
-        } else {
-          MD_CUDA_TRY(cudaLaunchKernel(sk, dim3(static_cast<unsigned>(g)), dim3(kArThreads), args,
-                                       smem, as_stream(stream)));
-        }
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        return MD_OK;
+        a.cfg_word = cfg_word_of(MD_ROUTE_STREAM, false, false, TE);
+        const void* k = allreduce_stream_kernel_of(epi);
+        int rc = smem_attr_once(k, dev, kStreamRingBytes);
+        if (rc == MD_OK)
+          rc = launch_views(k, g, n_views, static_cast<size_t>(S) * stage_bytes, &a, stream);
+        if (rc == MD_OK) record_route(dev, MD_ROUTE_STREAM, TE, false);
+        return rc;
       }
     }
   }
 
-  // owner-push kernel: plain buffers from push_min_bytes(N) up (MD_AR_PUSH=0
-  // disables it, =1 forces it); fused SGD calls opt-in (MD_AR_PUSH_FUSED=1)
-  // while the update range avoids the buffer's unaligned tail
-  const char* pe = getenv("MD_AR_PUSH");
-  const bool push_size = pe ? atoi(pe) != 0 : n * 4 >= push_min_bytes(N);
-  const bool push_fused = getenv("MD_AR_PUSH_FUSED") != nullptr;
-  if (push_size && (epi == 0 || (push_fused && update_len <= (n & ~int64_t(3)))) && N > 1 &&
-      n > 0 && n_workers == 0 && a.vec_ok && plan->prog_dev) {
-    // tile: deep enough rings for the N sources (measured, graph-timed 1 GiB:
-    // N = 4 2048 -> 2361 us vs 4096 -> 2596 us; N = 2 3072 -> 1615 vs 1636)
-    int64_t TE = N == 2 ? 3072 : 2048;
-    if (const char* te = getenv("MD_AR_TILE")) TE = std::max<int64_t>(4, atoll(te) & ~int64_t(3));
-    const int64_t n4 = n & ~int64_t(3);
-    const int64_t per = ((n4 / 4 + N - 1) / N) * 4;
-    while ((per + TE - 1) / TE > kMaxTiles) TE *= 2;
-    const int64_t stage_bytes = static_cast<int64_t>(N + 1) * TE * 4;
-    const int S = static_cast<int>(std::min<int64_t>(8, kRingBytes / stage_bytes));
-    const int avail = sm_count(dev) / n_views;
-    if (S >= 2 && avail >= 2) {
-      const int64_t T = std::max<int64_t>(1, (per + TE - 1) / TE);
-      int recv = 0;
-      if (epi != 0) {
-        recv = avail / 4;
-        if (const char* rc = getenv("MD_AR_PUSH_RECV")) recv = atoi(rc);
-        recv = std::max(1, std::min(recv, avail - 1));
-      }
-      const int g_own = static_cast<int>(std::min<int64_t>(avail - recv, T));
-      a.seg = TE;
-      a.lag = S;
-      a.max_stage = g_own;
-      a.ctas_per_view = g_own + recv;
-      a.prog = plan->prog_dev;
-      const void* pk = nullptr;
-      switch (epi) {
-        case 1: pk = (const void*)allreduce_push_kernel<1>; break;
-        case 2: pk = (const void*)allreduce_push_kernel<2>; break;
-        case 3: pk = (const void*)allreduce_push_kernel<3>; break;
-        case 4: pk = (const void*)allreduce_push_kernel<4>; break;
-        default: pk = (const void*)allreduce_push_kernel<0>; break;
-      }
-      static std::atomic<uint32_t> pk_set[64];
-      const uint32_t pbit = 1u << epi;
-      if (dev < 0 || dev >= 64 || !(pk_set[dev].load() & pbit)) {
-        MD_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kRingBytes)));
-        if (dev >= 0 && dev < 64) pk_set[dev].fetch_or(pbit);
-      }
-      const size_t smem = static_cast<size_t>(S) * stage_bytes;
-      const unsigned grid = static_cast<unsigned>(a.ctas_per_view);
-      void* args[] = {&a};
-      if (n_views > 1 || getenv("MD_AR_COOP")) {
-        MD_CUDA_TRY(cudaLaunchCooperativeKernel(pk, dim3(grid * n_views), dim3(kArThreads), args,
-                                                smem, as_stream(stream)));
-      } else {
-        MD_CUDA_TRY(cudaLaunchKernel(pk, dim3(grid), dim3(kArThreads), args, smem,
-                                     as_stream(stream)));
-      }
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      return MD_OK;
-    }
-  }
-
-  // owner-computes schedule (md_plan_set_schedule, build_owner_plans): the
-  // same channelized kernel over the owner plan (n slices), each owner
-  // evaluating the plan's fold programs. Worker folds and unaligned buffers
-  // keep the tree schedule (same bits either way).
+  // ---- the pipelined tree: every other call (fused updates at N > 2, worker
+  // folds, unaligned buffers). The owner-computes schedule
+  // (md_plan_set_schedule, build_owner_plans) runs the same channelized
+  // kernel over the owner plan (n slices), each owner evaluating the plan's
+  // fold programs; worker folds and unaligned buffers keep the tree schedule
+  // (same bits either way).
   auto weighted_of = [&](const std::vector<RankPlan>& plans) {
     int wmax = 0;
     for (const RankPlan& rp : plans) {
@@ -2801,19 +2783,17 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     }
     return wmax;
   };
-  const int est_ctas = sm_count(dev) / n_views;
   // (the owner plan needs the channelized kernel: one CTA per task at least)
   const bool owner = plan->schedule == MD_SCHED_OWNER && N > 1 && n_workers == 0 && a.vec_ok &&
-                     !getenv("MD_AR_QUEUE") && plan->owner_dev && plan->prog_dev &&
-                     weighted_of(plan->owner_host) <= est_ctas;
+                     req != MD_ROUTE_QUEUE && plan->owner_dev && plan->prog_dev &&
+                     weighted_of(plan->owner_host) <= avail;
   const std::vector<RankPlan>& hp = owner ? plan->owner_host : plan->host;
   if (owner) {
     a.plan = plan->owner_dev;
     a.k = N;
-    a.prog = plan->prog_dev;
-    a.prog_k = plan->k;
     const int64_t ml = (n + N - 1) / N;
-    const int64_t sg = std::min(std::max<int64_t>(4, (seg_elems + 3) & ~int64_t(3)), auto_seg(ml));
+    const int64_t sg =
+        std::min(std::max<int64_t>(4, (seg_elems + 3) & ~int64_t(3)), auto_seg(ml, dev));
     const int64_t ms = ((ml + 3) / kMaxSegs + 4 + 3) & ~int64_t(3);
     a.seg = std::max(sg, ms);
     int64_t mx2 = 0;
@@ -2824,30 +2804,17 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     }
     a.max_nseg = static_cast<int32_t>(mx2);
   }
-
   // 16-byte aligned buffers take the channelized TMA kernel; anything else
-  // the work-queue kernel with its scalar path (MD_AR_QUEUE=1 forces it)
+  // the work-queue kernel with its scalar path (MD_ROUTE_QUEUE forces it)
   // (and only when every task of every rank can own at least one CTA)
-  const int weighted = weighted_of(hp);
-  const bool chan = a.vec_ok && !getenv("MD_AR_QUEUE") && weighted <= est_ctas;
-  switch (epi) {
-    case 1: kern = chan ? (const void*)allreduce_channels_kernel<1> : (const void*)allreduce_kernel<1>; break;
-    case 2: kern = chan ? (const void*)allreduce_channels_kernel<2> : (const void*)allreduce_kernel<2>; break;
-    case 3: kern = chan ? (const void*)allreduce_channels_kernel<3> : (const void*)allreduce_kernel<3>; break;
-    case 4: kern = chan ? (const void*)allreduce_channels_kernel<4> : (const void*)allreduce_kernel<4>; break;
-    default: kern = chan ? (const void*)allreduce_channels_kernel<0> : (const void*)allreduce_kernel<0>; break;
-  }
-  // the attribute lives in each device's context: remember it per device
-  static std::atomic<uint32_t> smem_set[64];
-  const uint32_t bit = 1u << (epi + (chan ? 8 : 0));
-  if (dev < 0 || dev >= 64 || !(smem_set[dev].load() & bit)) {
-    MD_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kRingBytes)));
-    if (dev >= 0 && dev < 64) smem_set[dev].fetch_or(bit);
-  }
+  const bool chan = a.vec_ok && req != MD_ROUTE_QUEUE && weighted_of(hp) <= avail;
+  const void* kern = chan ? allreduce_channels_kernel_of(epi) : allreduce_kernel_of(epi);
+  int rc = smem_attr_once(kern, dev, kRingBytes);
+  if (rc != MD_OK) return rc;
+  int per_sm = 0;
   MD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArThreads,
                                                              kRingBytes));
-  int resident = per_sm * sm_count(dev);
+  const int resident = per_sm * sm_count(dev);
   if (ctas <= 0) ctas = resident / n_views;
   ctas = std::min(ctas, resident / n_views);
   if (ctas < 1) {
@@ -2861,15 +2828,12 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     max_tasks = std::max(max_tasks, rp.n_tasks);
     for (int i = 0; i < rp.n_tasks; ++i) max_stage = std::max(max_stage, rp.t[i].stage);
   }
-  int lag = std::max(1, ctas / max_tasks);
-  if (const char* e = getenv("MD_AR_LAG")) lag = std::max(0, atoi(e));
-  a.lag = lag;
+  a.lag = env.lag >= 0 ? env.lag : std::max(1, ctas / max_tasks);
   a.max_stage = max_stage;
+  // the queue and channelized kernels exchange the same per-segment flags
+  a.cfg_word = cfg_word_of(MD_ROUTE_TREE, owner, false, a.seg);
   a.trace = nullptr;
-  a.flag_gpu_fence = getenv("MD_AR_SYS_FENCE") == nullptr;  // see publish_flags
-  a.warp_fence = a.flag_gpu_fence && getenv("MD_AR_WARP_FENCE") != nullptr;
-  a.reverse_local = getenv("MD_AR_FORWARD") == nullptr;
-  if (getenv("MD_AR_TRACE")) {  // diagnostics: one event log per device, per call
+  if (env.trace) {  // diagnostics: one event log per device, per call
     const size_t bytes = sizeof(TraceEv) * 3 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
     if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
       if (g_trace[dev].ptr) cudaFree(g_trace[dev].ptr);
@@ -2881,24 +2845,9 @@ int md_allreduce(md_comm_t* const* comms, int32_t n_views, const md_plan_t* plan
     g_trace[dev].used = bytes;
     a.trace = static_cast<TraceEv*>(g_trace[dev].ptr);
   }
-  void* args[] = {&a};
-  // Emulated ranks wait on each other's CTAs on ONE device: a cooperative
-  // launch guarantees they are co-resident. A real rank's CTAs only wait on
-  // other GPUs (never on a sibling CTA), so a plain launch of <= one CTA per
-  // SM is deadlock-free there; MD_AR_COOP=1 forces the cooperative launch.
-  if (n_views > 1 || getenv("MD_AR_COOP")) {
-    MD_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(ctas * n_views), dim3(kArThreads), args,
-                                            kRingBytes, as_stream(stream)));
-  } else {
-    // programmatic dependent launch: the CTAs are scheduled while the
-    // predecessor drains and block in griddepcontrol.wait (md_common.cuh)
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute at[1];
-    pdl_config(&cfg, at, dim3(ctas), dim3(kArThreads), kRingBytes, as_stream(stream));
-    MD_CUDA_TRY(cudaLaunchKernelExC(&cfg, kern, args));
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return MD_OK;
+  rc = launch_views(kern, ctas, n_views, kRingBytes, &a, stream);
+  if (rc == MD_OK) record_route(dev, chan ? MD_ROUTE_TREE : MD_ROUTE_QUEUE, a.seg, false);
+  return rc;
 }
 
 }  // extern "C"

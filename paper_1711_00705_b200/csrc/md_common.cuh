@@ -63,42 +63,6 @@ inline void prefer_max_smem(K kernel, std::atomic<uint64_t>& done) {
 
 int sm_count(int device);
 
-// ---- programmatic dependent launch (PDL) -------------------------------------
-// The kernels of a training step (picks -> gather -> fill -> fused allreduce)
-// are launched with programmatic stream serialization: a kernel's CTAs may be
-// scheduled while its predecessor drains, run their prologue (SMEM tables,
-// mbarrier init), and block in pdl_wait() -- griddepcontrol.wait returns once
-// every prerequisite grid has COMPLETED and its writes are visible -- before
-// touching global memory. Every kernel launched this way calls pdl_wait()
-// before its first dependent access, so the ordering stays transitive along
-// the stream. Without the launch attribute both instructions are no-ops.
-// Opt-in (MD_PDL=1): on B200 it measured no gain for the allreduce (N = 2, 4:
-// +-1 %) and a loss in the N = 1 step (110 -> 129 us), profiles/README.md.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-bool pdl_enabled();
-inline void pdl_config(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* at, dim3 grid, dim3 block,
-                       size_t smem, cudaStream_t s) {
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg->gridDim = grid;
-  cfg->blockDim = block;
-  cfg->dynamicSmemBytes = smem;
-  cfg->stream = s;
-  cfg->attrs = at;
-  cfg->numAttrs = pdl_enabled() ? 1 : 0;
-}
-template <typename... KP, typename... A>
-inline cudaError_t launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              A... args) {
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[1];
-  pdl_config(&cfg, at, grid, block, smem, s);
-  return cudaLaunchKernelEx(&cfg, k, static_cast<KP>(args)...);
-}
-
 // ---- exact float32 arithmetic (no contraction: every op rounds once) --------
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),

@@ -129,8 +129,6 @@ __global__ void __launch_bounds__(1024) picks_step_kernel(uint64_t seed, uint64_
                                                           uint64_t worker, int64_t* step,
                                                           uint32_t n, int64_t batch,
                                                           int64_t* picks) {
-  pdl_wait();
-  pdl_launch_dependents();
   const int64_t st = *step;
   const uint64_t key =
       mix64_step(mix64_step(mix64_step(mix64_step(0, seed), role), worker),
@@ -505,8 +503,6 @@ __global__ void __launch_bounds__(512) gather_kernel(const uint8_t* blob, const 
                                                      int32_t* bad, int chunks) {
   // work unit = (record, chunk of kGatherChunk bytes): a 32-record batch of
   // 150 KB images spreads over ~150 CTAs instead of 32
-  pdl_wait();
-  pdl_launch_dependents();
   const int64_t units = batch * chunks;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t b = u / chunks;
@@ -526,113 +522,6 @@ __global__ void __launch_bounds__(512) gather_kernel(const uint8_t* blob, const 
   }
 }
 
-// Fixed-size gather on the TMA engines: each CTA (one warp, lane 0 issues)
-// owns a contiguous range of (record, 32 KiB chunk) units and streams them
-// through a ring of SMEM stages -- cp.async.bulk load (mbarrier) then
-// cp.async.bulk store -- so ~kGStages chunks per SM are in flight with no
-// register traffic; a record's metadata (picks -> off/len/label) is loaded
-// once per record. A record whose source is not 16-byte aligned is copied by
-// the warp directly. Opt-in (MD_GATHER_TMA=1): measured on B200 the LDG
-// kernel below is as fast for bulk gathers (6.3-6.5 vs 5.7-6.2 TB/s
-// read+write, tools/gather_probe.py) and faster for 32-record batches, where
-// its (record, chunk) units spread over more CTAs (5.9 vs 7.0 us).
-constexpr int kGStages = 6;
-
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-               "r"(smem_addr(ssrc)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-// wait until at most `pending` bulk store groups may still read their SMEM
-__device__ __forceinline__ void bulk_wait_read(uint32_t pending) {
-  switch (pending) {
-    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
-    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
-    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
-    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
-    default: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
-  }
-  static_assert(kGStages <= 6, "bulk_wait_read covers up to kGStages - 1 newer groups");
-}
-
-__global__ void __launch_bounds__(32, 1) gather_tma_kernel(
-    const uint8_t* blob, const uint64_t* off, const uint32_t* len, const uint32_t* label,
-    const int64_t* picks, int64_t batch, uint8_t* out, int64_t stride, uint32_t* out_label,
-    int32_t* bad, int chunks) {
-  extern __shared__ __align__(128) char gring[];
-  __shared__ __align__(8) uint64_t full[kGStages];
-  const int lane = threadIdx.x;
-  const int64_t units = batch * chunks;
-  const int64_t per = (units + gridDim.x - 1) / gridDim.x;
-  const int64_t u0 = static_cast<int64_t>(blockIdx.x) * per;
-  const int64_t u1 = min(units, u0 + per);
-  if (u0 >= u1) return;
-  if (lane == 0) {
-    for (int s = 0; s < kGStages; ++s) mbar_init(&full[s], 1);
-    mbar_init_fence();
-  }
-  __syncwarp();
-  uint8_t* pdst[kGStages];
-  uint32_t pbytes[kGStages];
-  int64_t cur_b = -1, next = u0;
-  const uint8_t* src = nullptr;
-  uint8_t* dst = nullptr;
-  uint32_t L = 0;
-  bool ok = false, aligned = false;
-  uint32_t issued = 0, stored = 0;  // ring sequence numbers
-  for (;;) {
-    while (next < u1 && issued - stored < kGStages) {
-      const int64_t b = next / chunks;
-      const int c = static_cast<int>(next % chunks);
-      ++next;
-      if (b != cur_b) {
-        cur_b = b;
-        const int64_t r = picks[b];
-        L = len[r];
-        src = blob + off[r];
-        dst = out + b * stride;
-        ok = static_cast<int64_t>(L) == stride;
-        aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-        if (lane == 0) {
-          if (!ok && bad) atomicExch(bad, 1);
-          if (ok && c == 0 && out_label) out_label[b] = label[r];
-        }
-      }
-      if (!ok) continue;
-      const uint64_t lo = static_cast<uint64_t>(c) * kGatherChunk;
-      if (lo >= L) continue;
-      const uint32_t n = static_cast<uint32_t>(min(static_cast<uint64_t>(kGatherChunk), L - lo));
-      if (!aligned || (n & 15)) {  // rare: plain warp copy
-        for (uint32_t k = lane; k < n; k += 32) dst[lo + k] = src[lo + k];
-        continue;
-      }
-      const uint32_t st = issued % kGStages;
-      if (lane == 0) {
-        if (issued >= kGStages) bulk_wait_read(stored - 1 - (issued - kGStages));
-        mbar_expect_tx(&full[st], n);
-        tma_load_1d(gring + st * kGatherChunk, src + lo, n, &full[st]);
-      }
-      pdst[st] = dst + lo;
-      pbytes[st] = n;
-      ++issued;
-    }
-    if (stored == issued) {
-      if (next >= u1) break;
-      continue;
-    }
-    const uint32_t st = stored % kGStages;
-    if (lane == 0) {
-      while (!mbar_try_wait(&full[st], (stored / kGStages) & 1)) {
-      }
-      bulk_store(pdst[st], gring + st * kGatherChunk, pbytes[st]);
-    }
-    ++stored;
-  }
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 
 struct SegCopy {
   uint8_t* dst[MD_MAX_GROUP];
@@ -816,8 +705,8 @@ int md_random_batch_step(uint64_t seed, uint64_t role, uint64_t worker, int64_t*
   }
   static std::atomic<uint64_t> carve{0};
   prefer_max_smem(picks_step_kernel, carve);
-  MD_CUDA_TRY(launch_pdl(picks_step_kernel, 1, 1024, 0, as_stream(stream), seed, role, worker,
-                         step, static_cast<uint32_t>(n_records), batch, picks));
+  picks_step_kernel<<<1, 1024, 0, as_stream(stream)>>>(seed, role, worker, step,
+                                                      static_cast<uint32_t>(n_records), batch, picks);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
@@ -832,28 +721,10 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
   }
   const int chunks =
       out_stride > 0 ? static_cast<int>((out_stride + kGatherChunk - 1) / kGatherChunk) : 1;
-  if (out_stride > 0 && (out_stride & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
-      getenv("MD_GATHER_TMA")) {
-    static std::atomic<uint32_t> attr_set[64];
-    int dev = 0;
-    MD_CUDA_TRY(cudaGetDevice(&dev));
-    constexpr int kSmem = kGStages * static_cast<int>(kGatherChunk);
-    if (dev < 0 || dev >= 64 || !attr_set[dev].exchange(1)) {
-      MD_CUDA_TRY(cudaFuncSetAttribute(gather_tma_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    }
-    const int64_t units = batch * chunks;
-    const int grid = static_cast<int>(std::min<int64_t>(units, sm_count(dev)));
-    gather_tma_kernel<<<grid, 32, kSmem, as_stream(stream)>>>(
-        blob, off, len, label, picks, batch, out, out_stride, out_label, err_flag, chunks);
-    MD_LAUNCH_CHECK();
-    return MD_OK;
-  }
   static std::atomic<uint64_t> carve{0};
   prefer_max_smem(gather_kernel, carve);
-  MD_CUDA_TRY(launch_pdl(gather_kernel, record_grid(batch * chunks), 512, 0, as_stream(stream),
-                         blob, off, len, label, picks, batch, out, out_stride, out_off, out_label,
-                         err_flag, chunks));
+  gather_kernel<<<record_grid(batch * chunks), 512, 0, as_stream(stream)>>>(
+      blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }

@@ -28,11 +28,6 @@ void set_error(const char* fmt, ...) {
   t_err = buf;
 }
 
-bool pdl_enabled() {
-  static const bool on = getenv("MD_PDL") != nullptr;
-  return on;
-}
-
 int sm_count(int device) {
   static int cached[64] = {0};
   if (device < 0 || device >= 64) return 148;
@@ -143,15 +138,12 @@ static int launch_sgd(float* w, const float* g, float* mom, int64_t n, float c, 
 // ---- fill pattern of bench.py:188-195 ----------------------------------------
 // The pattern has period 997: each CTA tabulates the 997 float32 values once
 // (same float64 expression, same rounding) and streams float4 stores.
-template <bool kStream>
 __global__ void __launch_bounds__(kThreads) fill_kernel(float* __restrict__ buf, int64_t n,
                                                         double scale) {
   __shared__ float tab[997];
   for (int k = threadIdx.x; k < 997; k += blockDim.x)
     tab[k] = __double2float_rn(__dmul_rn(static_cast<double>(k) + 1.0, scale));
   __syncthreads();
-  pdl_wait();  // the table is private; the buffer may still be read by the last step
-  pdl_launch_dependents();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t first = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if ((reinterpret_cast<uintptr_t>(buf) & 15) == 0) {
@@ -170,8 +162,7 @@ __global__ void __launch_bounds__(kThreads) fill_kernel(float* __restrict__ buf,
       x.z = tab[r];
       r = (r == 996) ? 0 : r + 1;
       x.w = tab[r];
-      if (kStream) __stcs(b4 + j, x);
-      else b4[j] = x;
+      b4[j] = x;
       r0 += dr;
       if (r0 >= 997) r0 -= 997;
     }
@@ -212,7 +203,7 @@ __global__ void stamp_kernel(uint64_t* dst) { *dst = md::globaltimer_ns(); }
 extern "C" {
 
 const char* md_last_error(void) { return t_err.c_str(); }
-int md_version(void) { return 1; }
+int md_version(void) { return 2; }
 uint64_t md_launch_count(void) { return g_launches.load(); }
 
 int md_add_f32(float* dst, int64_t n_dst, const float* src, int64_t n_src, void* stream) {
@@ -277,17 +268,11 @@ int md_fill_rank_input(float* buf, int64_t n, int32_t rank, int32_t n_ranks, voi
   if (n == 0) return MD_OK;
   // numpy: (rank + 1) * np.pi / n_ranks, evaluated left to right in float64
   double scale = (static_cast<double>(rank) + 1.0) * M_PI / static_cast<double>(n_ranks);
-  // plain stores by default: the gradient stays in L2 for the allreduce that
-  // reads it next (MD_FILL_STREAM=1: evict-first stores, the A/B switch)
-  static std::atomic<uint64_t> carve0{0}, carve1{0};
+  // plain stores: the gradient stays in L2 for the allreduce that reads it next
+  static std::atomic<uint64_t> carve{0};
   const int grid = grid_for((n + 3) / 4, kThreads);
-  if (getenv("MD_FILL_STREAM")) {
-    prefer_max_smem(fill_kernel<true>, carve1);
-    MD_CUDA_TRY(launch_pdl(fill_kernel<true>, grid, kThreads, 0, as_stream(stream), buf, n, scale));
-  } else {
-    prefer_max_smem(fill_kernel<false>, carve0);
-    MD_CUDA_TRY(launch_pdl(fill_kernel<false>, grid, kThreads, 0, as_stream(stream), buf, n, scale));
-  }
+  prefer_max_smem(fill_kernel, carve);
+  fill_kernel<<<grid, kThreads, 0, as_stream(stream)>>>(buf, n, scale);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }

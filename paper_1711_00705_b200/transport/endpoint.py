@@ -217,17 +217,24 @@ class CudaEndpoint:
         """Collective allocation of a peer-registered tensor (zeroed)."""
         t = torch.zeros(n, dtype=dtype, device=self.torch_device)
         torch.cuda.synchronize(self.torch_device)
-        return t, self.register(t)
+        view = self.register(t)
+        self._views[(t.data_ptr(), t.numel() * t.element_size())] = view
+        return t, view
 
     # -- plans --------------------------------------------------------------------------
-    def plan(self, tables, schedule: str = "tree") -> C.c_void_p:
-        """Device plan for fold tables (cached per tables object and schedule:
-        "tree" = the reference's per-color trees, "owner" = owner-computes
-        slices with the same fold order, md_plan_set_schedule)."""
-        fast = self._plans.get((id(tables), schedule))
+    def plan(self, tables, schedule: str = "tree", route: str = "auto",
+             tile: int = 0) -> C.c_void_p:
+        """Device plan for fold tables (cached per tables object, schedule and
+        route: "tree" = the reference's per-color trees, "owner" =
+        owner-computes slices with the same fold order, md_plan_set_schedule;
+        ``route``/``tile`` pin md_allreduce's kernel, md_plan_set_route)."""
+        opts = (schedule, route, int(tile))
+        fast = self._plans.get((id(tables), opts))
         if fast is not None and fast[0] is tables:
             return fast[1]
-        key = (tables.key(), schedule)
+        if route not in _lib.ROUTES or route == "local":
+            raise InvalidConfig(f"unknown allreduce route {route!r}")
+        key = (tables.key(), opts)
         p = self._plans.get(key)
         if p is None:
             p = C.c_void_p()
@@ -248,9 +255,21 @@ class CudaEndpoint:
                 )
                 sched = _lib.MD_SCHED_OWNER if schedule == "owner" else _lib.MD_SCHED_TREE
                 _lib.check(self.lib.md_plan_set_schedule(p, sched))
+                _lib.check(self.lib.md_plan_set_route(p, _lib.ROUTES[route], int(tile)))
             self._plans[key] = p
-        self._plans[(id(tables), schedule)] = (tables, p)
+        self._plans[(id(tables), opts)] = (tables, p)
         return p
+
+    def view_of(self, tensor: torch.Tensor) -> PeerView:
+        """Peer view of a tensor registered once (collective on first use, then
+        cached by address and size; the view keeps the tensor alive, so the
+        address cannot be recycled): the sharded update's weights."""
+        key = (tensor.data_ptr(), tensor.numel() * tensor.element_size())
+        v = self._views.get(key)
+        if v is None:
+            v = self.register(tensor)
+            self._views[key] = v
+        return v
 
     # -- errors / sync -------------------------------------------------------------------
     def take_error(self) -> None:

@@ -100,7 +100,44 @@ def main() -> None:
                 ep.take_error()
                 ok = ok and bool(np.array_equal(gb.data.cpu().numpy(), want2))
             out[f"graph_{name}"] = ok
-        # 5. alltoallv (host payloads, device exchange)
+        # 5. the C5 call at full size (25.6M + 2 floats, momentum + weight
+        #    decay), two calls back to back, on the default route of each update
+        #    mode (replicated: stream kernel at N = 2, tree above; sharded:
+        #    owner-push) -- md_last_route says which kernel ran
+        from paper_1711_00705_b200 import _lib
+
+        P5, L5 = 25_600_000, 25_600_002
+        src5 = [np.random.default_rng(77 + r).standard_normal(L5, dtype=np.float32)
+                for r in range(N)]
+        w5 = np.random.default_rng(78).standard_normal(P5, dtype=np.float32)
+        ts5 = build_multicolor_trees(N, ks[-1], 4)
+        g5 = O.fold_c(O.tables_from_trees(N, O.trees(N, ks[-1], 4)), src5)
+        c5, wd5 = float(np.float32(0.1 / (32 * N))), float(np.float32(1e-4 * 32 * N))
+        ww, mm = w5, np.zeros(P5, np.float32)
+        for _ in range(2):
+            ww, mm = O.sgd_np(ww, g5[:P5], mm.copy(), c5, 0.9, wd5)
+        want_route = {False: "stream" if N == 2 else "tree", True: "push"}
+        for sharded in (False, True):
+            w, _ = ep.alloc(P5)
+            w.copy_(torch.from_numpy(w5))
+            m = torch.zeros(P5, device=dev)
+            gb = GradientBuffer.alloc(L5, ep)
+            for _ in range(2):
+                gb.data.copy_(torch.from_numpy(src5[rank]))
+                allreduce(ep, gb, "multicolor", tree_set=ts5,
+                          update=SgdUpdate(weights=w, c=c5, momentum=m, mu=0.9, wd_b=wd5,
+                                           update_len=P5, sharded=sharded))
+            ep.synchronize()
+            route = _lib.last_route(ep.device)
+            tag = "sharded" if sharded else "replicated"
+            out[f"c5_{tag}_route"] = route[0] == want_route[sharded] and route[2] == sharded
+            out[f"c5_{tag}_w"] = bool(np.array_equal(w.cpu().numpy(), ww))
+            if not sharded:
+                out[f"c5_{tag}_g"] = bool(np.array_equal(gb.data.cpu().numpy(), g5))
+                out[f"c5_{tag}_m"] = bool(np.array_equal(m.cpu().numpy(), mm))
+            del w, m, gb
+        del src5, g5
+        # 6. alltoallv (host payloads, device exchange)
         mats = [[bytes([s, d]) * (s + d + 1) for d in range(N)] for s in range(N)]
         got = alltoallv(ep, VarPayload.from_slices(mats[rank])).data
         out["alltoallv"] = bytes(got) == b"".join(mats[s][rank] for s in range(N))

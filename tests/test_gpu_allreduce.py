@@ -25,25 +25,18 @@ from tests.test_oracle import GOLD_MC
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream", "push", "pushfused"])
+@pytest.fixture(autouse=True, params=["tree", "oneshot", "ll", "stream", "push"])
 def ar_path(request, monkeypatch):
-    """Every test runs on each kernel: the pipelined tree schedule
-    (allreduce_channels_kernel / the work-queue kernel), the one-shot pull
-    kernel, the LL push kernel, the tiled all-pull stream kernel and the
-    owner-push kernel (plain, and with the fused SGD update on receiver CTAs)
-    -- all but the tree evaluate the same fold programs locally, so the bits
-    must not change. (Calls a path cannot take -- worker folds, sizes beyond
-    a path's range -- fall through to the tree schedule.)"""
-    big = str(1 << 40)
-    p = request.param
-    monkeypatch.setenv("MD_AR_ONESHOT_MAX", big if p == "oneshot" else "0")
-    monkeypatch.setenv("MD_AR_LL_MAX", big if p == "ll" else "0")
-    monkeypatch.setenv("MD_AR_STREAM", "1" if p == "stream" else "0")
-    monkeypatch.setenv("MD_AR_PUSH", "1" if p in ("push", "pushfused") else "0")
-    if p == "pushfused":
-        monkeypatch.setenv("MD_AR_PUSH_FUSED", "1")
-    else:
-        monkeypatch.delenv("MD_AR_PUSH_FUSED", raising=False)
+    """Every test runs on each kernel route (md_plan_set_route): the pipelined
+    tree schedule (allreduce_channels_kernel / the work-queue kernel), the
+    one-shot pull kernel, the LL push kernel, the tiled all-pull stream kernel
+    and the owner-push kernel -- all but the tree evaluate the same fold
+    programs locally, so the bits must not change. (Calls a route cannot take
+    -- worker folds, sizes beyond its range, replicated updates on the push
+    route -- fall back to the tree schedule.)"""
+    from paper_1711_00705_b200 import collectives
+
+    monkeypatch.setattr(collectives, "_DEFAULT_ROUTE", request.param)
     return request.param
 
 
@@ -108,13 +101,11 @@ def test_back_to_back_calls_reuse_flags_safely():
 
 def test_oneshot_and_tree_calls_interleave(oracle, monkeypatch):
     """Default thresholds: a 16 KB buffer takes the LL kernel, a 4.8 MB one
-    the tree schedule; alternating them on one communicator keeps the
-    epoch protocol (arrival / done flags) consistent and the bits exact."""
-    monkeypatch.delenv("MD_AR_ONESHOT_MAX", raising=False)
-    monkeypatch.delenv("MD_AR_LL_MAX", raising=False)
-    monkeypatch.delenv("MD_AR_STREAM", raising=False)
-    monkeypatch.delenv("MD_AR_PUSH", raising=False)
-    monkeypatch.delenv("MD_AR_PUSH_FUSED", raising=False)
+    the owner-push kernel (N = 4); alternating them on one communicator keeps
+    the epoch protocol (arrival / done flags) consistent and the bits exact."""
+    from paper_1711_00705_b200 import collectives
+
+    monkeypatch.setattr(collectives, "_DEFAULT_ROUTE", "auto")
     n = 4
     ts = build_multicolor_trees(n, 4, 4)
     tables = oracle.tables_from_trees(n, oracle.trees(n, 4, 4))
@@ -250,8 +241,10 @@ def test_fused_accumulation_allreduce_and_update(oracle, n, k, arity, mu, wd):
 @pytest.mark.parametrize("case", ["mc_8_10007_4_4", "mc_4_4099_2_4", "mc_16_250_4_4"])
 def test_work_queue_kernel_matches_reference(golden, monkeypatch, case):
     """The work-queue kernel (fallback when the channel allotment does not
-    fit) folds identically; MD_AR_QUEUE=1 forces it."""
-    monkeypatch.setenv("MD_AR_QUEUE", "1")
+    fit) folds identically; the "queue" route forces it."""
+    from paper_1711_00705_b200 import collectives
+
+    monkeypatch.setattr(collectives, "_DEFAULT_ROUTE", "queue")
     n, _, k, arity = (int(x) for x in case.split("_")[1:])
     ts = build_multicolor_trees(n, k, arity)
     for r in run(n, list(golden[case + "_in"]), "multicolor", tree_set=ts, segment_elems=512):
@@ -411,3 +404,22 @@ def test_p2p_four_gpus_match_reference(golden, case):
         assert np.array_equal(r, golden[case + "_out"])
     out = run(4, list(golden["ring_4_4099_in"]), "ring", emulate=False)
     assert all(np.array_equal(o, golden["ring_4_4099_out"]) for o in out)
+
+
+@pytest.mark.multigpu
+@need_gpus(2)
+def test_ranks_on_different_routes_fail_together():
+    """Two ranks that take different kernels (here pinned: the tree and the
+    one-shot pull) must not exchange differently shaped flags: the entry
+    barrier compares their route words and both raise InvalidConfig."""
+    def prog(ep):
+        buf = GradientBuffer.alloc(100_000, ep)
+        try:
+            allreduce(ep, buf, "multicolor", tree_set=build_multicolor_trees(2, 1, 4),
+                      route="tree" if ep.rank == 0 else "oneshot")
+        except errors.InvalidConfig:
+            return "InvalidConfig"
+        return "ok"
+
+    assert run_ranks(2, "cuda", prog, emulate=False, pull_timeout=5.0).results == \
+        ["InvalidConfig", "InvalidConfig"]

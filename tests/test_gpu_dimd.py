@@ -185,10 +185,10 @@ def test_batch_stream_matches_keyed_batches_eager_and_graph():
 
 
 @pytest.mark.parametrize("lead", [0, 7])
-def test_fixed_size_gather_tma_path(monkeypatch, lead):
-    """The TMA gather (multi-chunk records, ragged last chunk, unaligned
-    sources after a 7-byte record, bad-length detection) byte-equal with the
-    host copy of the picked records and with the default LDG kernel."""
+def test_fixed_size_gather_multichunk_records(lead):
+    """The gather kernel on multi-chunk records (ragged last chunk, unaligned
+    sources after a 7-byte record) is byte-equal with the host copy of the
+    picked records, and a picked record of the wrong size raises on check()."""
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(11 + lead)
     L = 2 * 32768 + 1040  # three chunks, the last one ragged (multiple of 16)
@@ -198,7 +198,6 @@ def test_fixed_size_gather_tma_path(monkeypatch, lead):
     st = shard_from_bytes(blob, parse_index(idx), 0, 1, 1, device=dev)
     picks = torch.tensor([i + (1 if lead else 0) for i in rng.integers(0, 300, 700)],
                          dtype=torch.int64, device=dev)
-    monkeypatch.setenv("MD_GATHER_TMA", "1")
     slots = dimd.BatchSlots(700, L, dev)
     slots.picks.copy_(picks)
     dimd._gather_fixed(st, slots, 700, L)
@@ -207,22 +206,13 @@ def test_fixed_size_gather_tma_path(monkeypatch, lead):
     host = np.stack([np.frombuffer(recs[int(p)].bytes, np.uint8) for p in picks.cpu()])
     assert np.array_equal(slots.records.cpu().numpy(), host)
     assert slots.labels.cpu().tolist() == [recs[int(p)].label for p in picks.cpu()]
-    monkeypatch.delenv("MD_GATHER_TMA")
-    ldg = dimd.BatchSlots(700, L, dev)
-    ldg.picks.copy_(picks)
-    dimd._gather_fixed(st, ldg, 700, L)
-    assert torch.equal(ldg.records, slots.records)
-    if lead:  # a picked record of the wrong size raises on check(), both kernels
-        for tma in (True, False):
-            if tma:
-                monkeypatch.setenv("MD_GATHER_TMA", "1")
-            bad = dimd.BatchSlots(700, L, dev)
-            bad.picks.copy_(picks)
-            bad.picks[3] = 0
-            dimd._gather_fixed(st, bad, 700, L)
-            with pytest.raises(errors.LengthMismatch):
-                bad.check()
-            monkeypatch.delenv("MD_GATHER_TMA", raising=False)
+    if lead:
+        bad = dimd.BatchSlots(700, L, dev)
+        bad.picks.copy_(picks)
+        bad.picks[3] = 0
+        dimd._gather_fixed(st, bad, 700, L)
+        with pytest.raises(errors.LengthMismatch):
+            bad.check()
 
 
 @pytest.mark.parametrize("n", [2**31 + 1, 3 * 2**30, 160_000])

@@ -28,10 +28,10 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _owner_plan_only(monkeypatch):
-    monkeypatch.setenv("MD_AR_LL_MAX", "0")
-    monkeypatch.setenv("MD_AR_ONESHOT_MAX", "0")
-    monkeypatch.setenv("MD_AR_STREAM", "0")
-    monkeypatch.setenv("MD_AR_PUSH", "0")
+    """The owner plan runs on the channelized tree kernel: pin that route."""
+    from paper_1711_00705_b200 import collectives
+
+    monkeypatch.setattr(collectives, "_DEFAULT_ROUTE", "tree")
 
 
 def run(n, arrays, algo, emulate=True, **kw):

@@ -1,14 +1,15 @@
-"""The stream (all-pull, tiled) kernel as the DEFAULT route of fused N = 2
-calls at the C5 size (25.6M + 2 floats, momentum + weight decay): no kernel
-switch set, balanced tiles chosen by md_allreduce. Same bits as the oracle's
-fold + float32 update (the reference order: at N = 2 every color folds
-root + child, and the update is the oracle's sgd_np)."""
+"""The stream (all-pull, tiled) kernel as the DEFAULT route of replicated
+fused N = 2 calls at the C5 size (25.6M + 2 floats, momentum + weight decay):
+no route pinned, balanced tiles chosen by md_allreduce (and the test checks
+that the stream kernel is what ran). Same bits as the oracle's fold + float32
+update (the reference order: at N = 2 every color folds root + child, and the
+update is the oracle's sgd_np)."""
 
 import numpy as np
 import pytest
 import torch
 
-from paper_1711_00705_b200 import GradientBuffer, build_multicolor_trees, run_ranks
+from paper_1711_00705_b200 import GradientBuffer, _lib, build_multicolor_trees, run_ranks
 from paper_1711_00705_b200.collectives import SgdUpdate, allreduce
 from tests.conftest import need_gpus
 
@@ -20,9 +21,9 @@ P = L - 2
 
 @pytest.fixture(autouse=True)
 def default_route(monkeypatch):
-    for var in ("MD_AR_STREAM", "MD_AR_TILE", "MD_AR_PUSH", "MD_AR_PUSH_FUSED",
-                "MD_AR_ONESHOT_MAX", "MD_AR_LL_MAX"):
-        monkeypatch.delenv(var, raising=False)
+    from paper_1711_00705_b200 import collectives
+
+    monkeypatch.setattr(collectives, "_DEFAULT_ROUTE", "auto")
 
 
 def _case(oracle, k, seed):
@@ -45,7 +46,8 @@ def _prog(arrays, w0, m0, ts, steps=1):
             buf = GradientBuffer(torch.from_numpy(arrays[ep.rank].copy()).to(dev))
             upd = SgdUpdate(weights=w, c=1e-3, momentum=m, mu=0.9, wd_b=3.2e-3, update_len=P)
             allreduce(ep, buf, "multicolor", tree_set=ts, update=upd)
-        return buf.data.cpu().numpy(), w.cpu().numpy(), m.cpu().numpy()
+        route = _lib.last_route(ep.device)
+        return buf.data.cpu().numpy(), w.cpu().numpy(), m.cpu().numpy(), route
 
     return prog
 
@@ -54,7 +56,8 @@ def _prog(arrays, w0, m0, ts, steps=1):
 def test_c5_size_fused_emulated(oracle, k):
     arrays, w0, m0, want, want_w, want_m = _case(oracle, k, 11 + k)
     ts = build_multicolor_trees(2, k, 4)
-    for g, w, m in run_ranks(2, "cuda", _prog(arrays, w0, m0, ts), emulate=True).results:
+    for g, w, m, route in run_ranks(2, "cuda", _prog(arrays, w0, m0, ts), emulate=True).results:
+        assert route[0] == "stream"
         assert np.array_equal(g, want)
         assert np.array_equal(w, want_w)
         assert np.array_equal(m, want_m)
@@ -68,7 +71,9 @@ def test_c5_size_fused_two_gpus_back_to_back(oracle):
     w1, m1 = oracle.sgd_np(w0, want[:P], m0.copy(), 1e-3, 0.9, 3.2e-3)
     w2, m2 = oracle.sgd_np(w1, want[:P], m1.copy(), 1e-3, 0.9, 3.2e-3)
     ts = build_multicolor_trees(2, 2, 4)
-    for g, w, m in run_ranks(2, "cuda", _prog(arrays, w0, m0, ts, steps=2), emulate=False).results:
+    for g, w, m, route in run_ranks(2, "cuda", _prog(arrays, w0, m0, ts, steps=2),
+                                    emulate=False).results:
+        assert route[0] == "stream"
         assert np.array_equal(g, want)
         assert np.array_equal(w, w2)
         assert np.array_equal(m, m2)

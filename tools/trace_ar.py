@@ -3,7 +3,9 @@
 per-CTA timeline: kernel span, producer flag waits, first-chunk latency,
 segment processing time and publish latency, grouped by task.
 
-    torchrun --nproc-per-node N tools/trace_ar.py [--seg 32768] [--plain]
+    MD_AR_TRACE=1 torchrun --nproc-per-node N tools/trace_ar.py [--seg 32768] [--plain]
+
+(MD_AR_TRACE is read once per process, so every call of the run is traced.)
 """
 
 from __future__ import annotations
@@ -130,7 +132,7 @@ def main() -> None:
             if i == 1:  # every later call overwrites the log: the last one is steady state
                 torch.cuda.synchronize(dev)
                 ep.barrier()
-                os.environ["MD_AR_TRACE"] = "1"
+                pass  # MD_AR_TRACE is read once per process: set it before launch
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(ep.stream)
             if i == 5:
@@ -142,7 +144,6 @@ def main() -> None:
             e1.record(ep.stream)
         torch.cuda.synchronize(dev)
         ms = e0.elapsed_time(e1)
-        os.environ.pop("MD_AR_TRACE")
         plain_ms = []
         for _ in range(5):  # untraced calls on the same stream, for comparison
             lib.md_fill_rank_input(grad.data.data_ptr(), P + 2, rank, N, _lib.stream_ptr(ep.stream))
