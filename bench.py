@@ -253,7 +253,11 @@ def run_ours(a) -> None:
         want_picks = random_batch_picks(store, BatchRequest(BATCH, key0))
         if not torch.equal(bslots[0].picks, want_picks):
             raise SystemExit("device-keyed batch stream diverged from random_batch")
-        idx = np.arange(0, P, 7919)
+        lo, hi = 0, P
+        if a.update == "sharded" and N > 1:  # the sum is kept on the own slice only
+            per = (((P + 2) // 4 + N - 1) // N) * 4
+            lo, hi = min(P, rank * per), min(P, (rank + 1) * per)
+        idx = np.arange(lo, hi, 7919)
         got = grad.data[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
         total = sum((r + 1) * np.pi / N for r in range(N))
         want = (idx.astype(np.float64) % 997.0 + 1.0) * total
@@ -316,7 +320,9 @@ def run_ours(a) -> None:
             from tools.linkmon import LinkMonitor
 
             mon = LinkMonitor.create(ep.device)
-            if mon is not None:
+            if mon is None:
+                link = {"error": f"NVML GPM: {LinkMonitor.last_error}"}
+            else:
                 ep.barrier()
                 torch.cuda.synchronize(dev)
                 mon.start()
@@ -495,8 +501,9 @@ def _link_summary(rows, n: int, ar_ms: float):
         return None
     links = [r[4] for r in rows]
     if any(x is None or "error" in x for x in links):
-        return {"error": "NVML GPM counters unavailable",
-                "detail": [x.get("error") if x else None for x in links]}
+        return {"error": "NVML GPM link counters unavailable on this box; NVLink bytes per "
+                         "call come from the ncu nvlrx/nvltx capture in profiles/",
+                "detail": [x.get("error") if x else None for x in links][:1]}
     calls = links[0]["allreduce_calls"]
     rx = [x["rx_bytes"] / calls for x in links]
     tx = [x["tx_bytes"] / calls for x in links]

@@ -49,6 +49,10 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=2017)
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--epochs", type=int, default=5)
+    ap.add_argument("--exchange", choices=["push", "pull"], default="push",
+                    help="shuffle data movement (dimd.EXCHANGE)")
+    ap.add_argument("--cpu-records", type=int, default=1024,
+                    help="records per member of the host (CPU reference) shuffle row; 0 = none")
     a = ap.parse_args()
 
     import torch
@@ -61,6 +65,7 @@ def main() -> None:
 
     ep = init_from_env()
     N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
+    dimd.EXCHANGE = a.exchange
     S, n = N, a.records
     # epoch keys _mix64(seed, "shuf", epoch), sgd.py:503-506
     with torch.cuda.stream(ep.stream):
@@ -126,8 +131,18 @@ def main() -> None:
         torch.cuda.synchronize(dev)
         bulk.check()
         bulk_ms = b0.elapsed_time(b1) / 5
+        # the gather kernel alone (picks already drawn): its HBM roofline
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(ep.stream)
+        for i in range(5):
+            dimd._gather_fixed(out, bulk, a.bulk, REC)
+        k1.record(ep.stream)
+        torch.cuda.synchronize(dev)
+        bulk.check()
+        gather_only_ms = k0.elapsed_time(k1) / 5
         del bulk
-    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases_all, walls, bulk_ms))
+    rows = ep.all_gather((wall, ev_ms, n_out, bad, exact, gather_ms, phases_all, walls, bulk_ms,
+                          gather_only_ms))
     if rank == 0:
         wall = max(r[0] for r in rows)
         total = sum(r[2] for r in rows)
@@ -149,19 +164,59 @@ def main() -> None:
             "batch32_ms": max(r[5] for r in rows),
             "batch32_is": "BatchStream.next() (picks + gather), 100 per CUDA graph, device time",
             "batch32_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
+            "exchange": a.exchange,
             "bulk_gather_records": a.bulk,
+            "bulk_gather_is": "random_batch_device: Philox picks of --bulk records + gather kernel",
             "bulk_gather_ms": max(r[8] for r in rows),
+            "gather_kernel_ms": max(r[9] for r in rows),
+            "gather_kernel_is": "md_gather alone on the same picks (2 x record bytes per record)",
+            "gather_kernel_hbm_GBps": 2 * a.bulk * REC / (max(r[9] for r in rows) / 1e3) / 1e9,
             "bulk_gather_records_per_s_per_gpu": a.bulk / (max(r[8] for r in rows) / 1e3),
             "bulk_gather_hbm_GBps": 2 * a.bulk * REC / (max(r[8] for r in rows) / 1e3) / 1e9,
         }
         peak = _hbm_peak()
         if peak:
             line["bulk_gather_hbm_frac"] = line["bulk_gather_hbm_GBps"] / peak[0]
+            line["gather_kernel_hbm_frac"] = line["gather_kernel_hbm_GBps"] / peak[0]
             line["hbm_peak"] = {"GBps": peak[0], "source": peak[1]}
         if rows[0][6] and rows[0][6][-1]:
             line["phases_s_per_rank"] = [r[6] for r in rows]
+        if a.cpu_records > 0:
+            line["cpu_baseline"] = cpu_shuffle(S, a.cpu_records, a.seed)
         print(json.dumps(line), flush=True)
     ep.barrier()
+
+
+def cpu_shuffle(S: int, n_local: int, seed: int, seconds: float = 5.0) -> dict:
+    """The reference algorithm of one shuffle epoch on the host, for a scaled
+    corpus (S members x n_local records of 224x224x3 bytes): every receiver's
+    plan with the oracle's C port of dimd.py:281-350 (numpy-Philox dest draws,
+    receive order, permutation), then the bytes moved into each receiver's new
+    blob (numpy take). Single thread. The reference itself (Python over its
+    threads transport) measured 2,337 records/s for 8,192 records at N = 8 in
+    the build container."""
+    import os
+
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(seed)
+    blobs = [rng.integers(0, 256, size=(n_local, REC), dtype=np.uint8) for _ in range(S)]
+    m_seg = 4
+    key = O.mix64(seed, O.SHUF_ROLE, 0)
+    t0, reps = time.perf_counter(), 0
+    while reps < 2 or time.perf_counter() - t0 < seconds:
+        for r in range(S):
+            mem, rec = O.shuffle_plan_c(key, 0, S, r, r, m_seg, [n_local] * S)
+            out = np.empty((len(mem), REC), np.uint8)
+            for q in range(S):
+                sel = mem == q
+                out[sel] = np.take(blobs[q], rec[sel], axis=0)
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": S * n_local / dt, "unit": "records/s (whole job)", "cores": 1,
+            "kind": "port", "affinity_cores": len(os.sched_getaffinity(0)),
+            "sample": f"one epoch of {S} x {n_local} records (150,528 B) on the host, "
+                      f"oracle C plan + numpy byte moves, {reps} repetitions"}
 
 
 if __name__ == "__main__":

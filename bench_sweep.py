@@ -13,10 +13,26 @@ events around each of R replays, median / G, max over ranks. Scenario
 each library's launch path (Python + ctypes / torch.distributed). Bus
 bandwidth = 2 * bytes * (N-1)/N / t (src/bench.py:116-119).
 Unconstructible (N, k, arity) triples are skipped like src/bench.py:224-232.
-At N >= 4, for k < N and sizes above the LL range, rows "..._owner" time the
-owner-computes schedule (same fold order, same bits; md_plan_set_schedule).
-Writes the reference's CSV schema to profiles/sweep_n{N}.csv (algorithm
-column carries k and arity) and prints one JSON line per row.
+
+Every row names its DATA MOVEMENT (all of them produce the reference's bits):
+  tree_k{k}_a{a}    the reference's schedule: reduce up + broadcast down each
+                    color's own tree (route pinned to the pipelined tree kernel,
+                    md_plan_set_route(MD_ROUTE_TREE)) -- the row whose speed
+                    depends on k and the tree shapes (SURVEY.md section 8d);
+  owner_k{k}_a{a}   owner-computes schedule on the same kernel (N >= 4, k < N;
+                    md_plan_set_schedule): every element still folds in its
+                    color's tree order;
+  push              owner-push kernel (sizes from 1 MiB; independent of k: it
+                    evaluates each element's color program, so one row, k = max);
+  auto_k{k}_a{a}    what a caller gets by default (route picked by size);
+                    the "route" column says which kernel md_allreduce ran
+                    (md_last_route: ll / oneshot / tree / push);
+  nccl_allreduce    NCCL 2.28 (torch.distributed) on the same buffer;
+  cpu_port_k{k}     the reference algorithm on the host (the oracle's threaded
+                    C port of the tree fold + broadcast, all host cores), sizes
+                    up to --cpu-max-mb; `cores` column.
+Writes the reference's CSV schema plus route/cores columns to
+profiles/sweep_n{N}.csv and prints one JSON line per row.
 """
 
 from __future__ import annotations
@@ -33,7 +49,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CSV_HEADER = "scenario,algorithm,n_ranks,payload_bytes,median_time_s,throughput_GBps,backend"
+CSV_HEADER = ("scenario,algorithm,n_ranks,payload_bytes,median_time_s,throughput_GBps,backend,"
+              "route,cores")
 
 
 def main() -> None:
@@ -44,7 +61,10 @@ def main() -> None:
     ap.add_argument("--seg", type=int, default=0, help="segment_elems (0 = library default)")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--graph-calls", type=int, default=20, help="calls per captured graph")
-    ap.add_argument("--no-eager", action="store_true", help="graph-timed rows only")
+    ap.add_argument("--eager", action="store_true", help="also host-launched (eager) rows")
+    ap.add_argument("--cpu-max-mb", type=int, default=128,
+                    help="largest payload of the CPU rows (0 = none)")
+    ap.add_argument("--cpu-seconds", type=float, default=3.0)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
 
@@ -142,40 +162,40 @@ def main() -> None:
         if bad > 1e-5:
             raise SystemExit(f"{name} n={n}: result check failed (max rel {bad:.3g})")
 
+    def measure(label, fn, n, size):
+        fill(n)
+        fn(n)
+        torch.cuda.synchronize(dev)
+        ep.take_error()
+        check(n, label)
+        route = _lib.last_route(ep.device)
+        rname = route[0] + ("_sharded" if route[2] else "")
+        t = timed_graph(fn, n)
+        if t is not None:
+            rows.append(("allreduce", label, N, size, t, "b200", rname, ""))
+        if a.eager:
+            t = timed(fn, n)
+            rows.append(("allreduce_eager", label, N, size, t, "b200", rname, ""))
+
     with torch.cuda.stream(stream):
         for size in sizes:
             n = size // 4
             view = GradientBuffer(buf.data[:n], peers=buf.peers)
             for k, arity, ts in plans:
-                def ours(n, ts=ts, view=view):
-                    allreduce(ep, view, "multicolor", tree_set=ts, segment_elems=seg, check=False)
+                def call(n, ts=ts, view=view, **kw):
+                    allreduce(ep, view, "multicolor", tree_set=ts, segment_elems=seg, check=False,
+                              **kw)
 
-                fill(n)
-                ours(n)
-                torch.cuda.synchronize(dev)
-                ep.take_error()
-                check(n, f"multicolor k={k}")
-                t = timed_graph(ours, n)
-                if t is not None:
-                    rows.append(("allreduce", f"multicolor_k{k}_a{arity}", N, size, t, "b200"))
-                if not a.no_eager:
-                    t = timed(ours, n)
-                    rows.append(("allreduce_eager", f"multicolor_k{k}_a{arity}", N, size, t, "b200"))
+                if N > 1:
+                    measure(f"tree_k{k}_a{arity}", lambda n, c=call: c(n, route="tree"), n, size)
                 if N >= 4 and k < N and size > (1 << 20):
-                    # owner-computes schedule: same fold order (same bits), balanced traffic
-                    def owner(n, ts=ts, view=view):
-                        allreduce(ep, view, "multicolor", tree_set=ts, segment_elems=seg,
-                                  check=False, schedule="owner")
-
-                    fill(n)
-                    owner(n)
-                    torch.cuda.synchronize(dev)
-                    ep.take_error()
-                    check(n, f"multicolor k={k} owner")
-                    t = timed_graph(owner, n)
-                    if t is not None:
-                        rows.append(("allreduce", f"multicolor_k{k}_a{arity}_owner", N, size, t,
-                                     "b200"))
+                    measure(f"owner_k{k}_a{arity}",
+                            lambda n, c=call: c(n, route="tree", schedule="owner"), n, size)
+                measure(f"auto_k{k}_a{arity}", call, n, size)
+            if N > 1 and size >= (1 << 20) and plans:
+                k, arity, ts = plans[-1]
+                measure("push", lambda n, ts=ts, view=view: allreduce(
+                    ep, view, "multicolor", tree_set=ts, check=False, route="push"), n, size)
             if nccl is not None:
                 def ref(n):
                     dist.all_reduce(buf.data[:n], group=nccl)
@@ -186,25 +206,60 @@ def main() -> None:
                 check(n, "nccl")
                 t = timed_graph(ref, n)
                 if t is not None:
-                    rows.append(("allreduce", "nccl_allreduce", N, size, t, "nccl"))
-                if not a.no_eager:
+                    rows.append(("allreduce", "nccl_allreduce", N, size, t, "nccl", "nccl", ""))
+                if a.eager:
                     t = timed(ref, n)
-                    rows.append(("allreduce_eager", "nccl_allreduce", N, size, t, "nccl"))
+                    rows.append(("allreduce_eager", "nccl_allreduce", N, size, t, "nccl", "nccl",
+                                 ""))
+
+    # the reference algorithm on the host CPU (rank 0; after the GPU rows)
+    if rank == 0 and a.cpu_max_mb > 0 and N > 1:
+        rows.extend(cpu_rows(N, [x for x in sizes if x <= a.cpu_max_mb << 20], plans,
+                             a.cpu_seconds))
+    ep.barrier()
 
     if rank == 0:
         out = Path(a.out) if a.out else ROOT / "profiles" / f"sweep_n{N}.csv"
         out.parent.mkdir(exist_ok=True)
         lines = [CSV_HEADER]
-        for sc, algo, n_r, size, t, be in rows:
+        for sc, algo, n_r, size, t, be, route, cores in rows:
             bus = 2 * size * (n_r - 1) / n_r / t / 1e9 if n_r > 1 else 0.0
-            lines.append(f"{sc},{algo},{n_r},{size},{t!r},{bus!r},{be}")
+            lines.append(f"{sc},{algo},{n_r},{size},{t!r},{bus!r},{be},{route},{cores}")
             print(json.dumps({"scenario": sc, "algorithm": algo, "n": n_r, "bytes": size,
-                              "us": t * 1e6,
-                              "bus_GBps": bus, "backend": be}), flush=True)
+                              "us": t * 1e6, "bus_GBps": bus, "backend": be, "route": route,
+                              "cores": cores}), flush=True)
         out.write_text("\n".join(lines) + "\n")
     ep.barrier()
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def cpu_rows(N, sizes, plans, seconds):
+    """The reference's CPU allreduce (tree fold + broadcast per color) for N
+    ranks on this host: the oracle's threaded C port (oracle/mdoracle.c
+    mo_allreduce_threads), all host cores, bounded to ~`seconds` per row."""
+    import time
+
+    from oracle import oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    out = []
+    for k, arity, _ in plans:
+        tables = O.tables_from_trees(N, O.trees(N, k, arity))
+        for size in sizes:
+            n = size // 4
+            bufs = [O.fill_rank_input(n, r, N) for r in range(N)]
+            O.allreduce_threads(tables, bufs, threads=cores)  # warm
+            t0, reps = time.perf_counter(), 0
+            while reps < 3 or time.perf_counter() - t0 < seconds:
+                O.allreduce_threads(tables, bufs, threads=cores)
+                reps += 1
+                if reps >= 1000:
+                    break
+            t = (time.perf_counter() - t0) / reps
+            out.append(("allreduce", f"cpu_port_k{k}_a{arity}", N, size, t, "cpu", "host",
+                        str(cores)))
+    return out
 
 
 if __name__ == "__main__":

@@ -283,6 +283,23 @@ int md_shuffle_pull(int32_t S, const uint8_t* const* peer_blob, const uint64_t* 
                     const uint64_t* out_off, const uint32_t* out_len, uint8_t* out_blob,
                     void* stream);
 
+/* The same exchange as stores (the default): md_shuffle_sendlist, on the
+ * RECEIVER, groups its output slots by source member into `list` (n_final
+ * entries of 24 bytes: {int64 source record, uint64 output offset, uint32
+ * length, uint32 source member}, slot order kept within a member) and writes
+ * begin[0..S] (device int64: member q's entries are list[begin[q] ..
+ * begin[q+1])). md_shuffle_push, on every SOURCE member, reads its own range
+ * of every receiver's list (peer-mapped) and stores those records from its
+ * local blob (blob + off[record]) into the receivers' new blobs (peer_out).
+ * Callers order the two with a barrier (every list complete before any push)
+ * and finish with one (every push landed before a receiver reads its blob). */
+int md_shuffle_sendlist(int32_t S, const int32_t* final_member, const int64_t* final_rec,
+                        int64_t n_final, const uint64_t* out_off, const uint32_t* out_len,
+                        void* list, int64_t* begin, void* stream);
+int md_shuffle_push(int32_t S, int32_t member, const uint8_t* blob, const uint64_t* off,
+                    const void* const* peer_list, const int64_t* const* peer_begin,
+                    uint8_t* const* peer_out, void* stream);
+
 /* alltoallv data movement (collectives.py:475-525): copy n_seg byte ranges,
  * dst[i] <- src[i] (len[i] bytes), src typically peer-mapped. Host arrays of
  * at most MD_MAX_GROUP entries. */

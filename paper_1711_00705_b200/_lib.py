@@ -97,6 +97,8 @@ SIGNATURES = {
         C.c_int, [_i32, _pp, _pp, _vp, _vp, _i64, _vp, _vp, _vp, C.POINTER(_u64), _vp]
     ),
     "md_shuffle_pull": (C.c_int, [_i32, _pp, _pp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "md_shuffle_sendlist": (C.c_int, [_i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "md_shuffle_push": (C.c_int, [_i32, _i32, _vp, _vp, _pp, _pp, _pp, _vp]),
     "md_copy_segments": (C.c_int, [_i32, _pp, _pp, C.POINTER(_u64), _vp]),
     "md_synth_records": (
         C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _u64, C.c_uint32, _vp]

@@ -2667,6 +2667,11 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
       int64_t TE = tile_req ? tile_req : (N == 2 ? 3072 : 2048);
       int64_t A0, B0;
       push_slice(n, N, 0, &A0, &B0);
+      if (!tile_req) {  // balanced: every CTA gets the same number of tiles (no ragged last wave)
+        const int64_t rounds = std::max<int64_t>(1, (B0 - A0 + avail * TE - 1) / (avail * TE));
+        TE = std::max<int64_t>(4, ((B0 - A0 + avail * rounds - 1) / (avail * rounds) + 3) &
+                                      ~int64_t(3));
+      }
       while ((B0 - A0 + TE - 1) / TE > kMaxTiles) TE *= 2;
       const int ups = epi == 0 ? 0 : (epi >= 3 ? 2 : 1);
       const int64_t stage_bytes = static_cast<int64_t>(N + 1 + ups) * TE * 4;

@@ -10,9 +10,10 @@ hot operations run on device, bit-exact with the reference's numpy Philox:
   reference-shaped ``random_batch`` copies Records to the host for parity);
 * ``shuffle_all`` / ``shuffle_group`` (dimd.py:261-350): destination draws of
   every member recomputed locally, receive order + final permutation
-  resolved before any byte moves (md_shuffle_plan), then each record is
-  pulled once, over NVLink, from its source member's blob into its final
-  slot (md_shuffle_pull);
+  resolved before any byte moves (md_shuffle_plan), then each record crosses
+  NVLink once, straight into its final slot: pushed by its source member
+  (md_shuffle_sendlist + md_shuffle_push, the default) or pulled by its
+  receiver (md_shuffle_pull, ``EXCHANGE = "pull"``);
 * ``shard_from_bytes`` / ``load_partition`` (dimd.py:166-207): striping rule
   ``i mod group_size == rank_in_group`` applied on the host index, records
   staged into HBM once.
@@ -468,6 +469,10 @@ def _group_counts(rows, members, m_segments: int) -> list[int]:
 
 
 LAST_SHUFFLE_PHASES: dict[str, float] = {}
+# how the shuffle's bytes cross the links: "push" (sources store records into
+# the receivers' new blobs, md_shuffle_push) or "pull" (receivers load them,
+# md_shuffle_pull). Same placement, same bytes.
+EXCHANGE = "push"
 
 
 class _ShardArena:
@@ -496,7 +501,7 @@ class _ShardArena:
         elif free:
             slot = max(free, key=lambda s: 0 if s[0] is None else s[0].numel())
         else:
-            slot = [None, None, None]
+            slot = [None, None, None, None]
             self.slots.append(slot)
         if slot[2] is None or slot[2].numel() < need:
             slot[2] = None
@@ -515,6 +520,17 @@ class _ShardArena:
             slot[0] = torch.empty(max(1, int(nbytes * self.HEADROOM)), dtype=torch.uint8,
                                   device=device)
         return slot[0][: max(1, nbytes)]
+
+    def sendlist(self, slot: list, n_final: int, S: int, device):
+        """The receiver's send list (24-byte entries, md_shuffle_sendlist) and
+        its begin[S + 1] array, in one peer-registrable allocation per slot."""
+        need = 24 * max(1, n_final) + 8 * (S + 1)
+        if slot[3] is None or slot[3].numel() < need:
+            slot[3] = None
+            slot[3] = torch.empty(int(need * self.HEADROOM) + 64, dtype=torch.uint8,
+                                  device=device)
+        raw = slot[3]
+        return raw, raw[: 24 * max(1, n_final)], raw[24 * max(1, n_final): need].view(torch.int64)
 
     @staticmethod
     def bind(slot: list, store) -> None:
@@ -608,16 +624,36 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     )
     mark("index")
     blob = arena.blob(slot, int(total.value), dev)
-    _lib.check(
-        lib.md_shuffle_pull(
-            S, _lib.ptr_array([v_blob.ptrs[m] for m in members]),
-            _lib.ptr_array([v_off.ptrs[m] for m in members]), fm.data_ptr(), fr.data_ptr(),
-            n_final, off.data_ptr(), ln.data_ptr(), blob.data_ptr(), s,
+    if EXCHANGE == "push":
+        # receiver side: our output slots grouped by source member; then one
+        # host collective publishes (new blob, send list) to every source
+        raw, lst, begin = arena.sendlist(slot, n_final, S, dev)
+        _lib.check(lib.md_shuffle_sendlist(S, fm.data_ptr(), fr.data_ptr(), n_final,
+                                           off.data_ptr(), ln.data_ptr(), lst.data_ptr(),
+                                           begin.data_ptr(), s))
+        torch.cuda.current_stream(dev).synchronize()  # lists complete before peers read them
+        (v_out, v_list), _ = ep.register_varlen_many([blob, raw])
+        mark("sendlist")
+        lst_ptrs = [v_list.ptrs[m] for m in members]
+        beg_ptrs = [p + (begin.data_ptr() - raw.data_ptr()) for p in lst_ptrs]
+        _lib.check(lib.md_shuffle_push(
+            S, store.rank_in_group, store.blob.data_ptr(),
+            (store.off if not empty else arrays[1]).data_ptr(),
+            _lib.ptr_array(lst_ptrs), _lib.ptr_array(beg_ptrs),
+            _lib.ptr_array([v_out.ptrs[m] for m in members]), s))
+    else:
+        _lib.check(
+            lib.md_shuffle_pull(
+                S, _lib.ptr_array([v_blob.ptrs[m] for m in members]),
+                _lib.ptr_array([v_off.ptrs[m] for m in members]), fm.data_ptr(), fr.data_ptr(),
+                n_final, off.data_ptr(), ln.data_ptr(), blob.data_ptr(), s,
+            )
         )
-    )
     torch.cuda.current_stream(dev).synchronize()
-    mark("pull")
-    ep.barrier()  # every pull from our old shard is done before anyone frees it
+    mark(EXCHANGE)
+    # pull: every read of our old shard is done before anyone frees it;
+    # push: every record pushed into our new blob has landed
+    ep.barrier()
     mark("barrier")
     out = ShardStore(blob, off[:n_final], ln[:n_final], lb[:n_final], store.group_id, S,
                      store.rank_in_group)

@@ -68,7 +68,9 @@ def main() -> None:
         for epoch in range(2):
             key = O.mix64(11, O.SHUF_ROLE, epoch)
             counts = ep.all_gather(store.n_records)
+            dimd.EXCHANGE = "push" if epoch == 0 else "pull"  # both data movements
             new = dimd.shuffle_all(ep, store, m_segments=3, seed=key)
+            dimd.EXCHANGE = "push"
             bad, gids = dimd.synth_verify(new, 11)
             mem, rec = O.shuffle_plan_c(key, 0, N, rank, rank, 3, counts)
             out[f"shuffle{epoch}_bytes"] = int(bad) == 0

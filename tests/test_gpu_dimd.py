@@ -64,8 +64,16 @@ def test_random_batch_large_n_and_fixed_size_gather(oracle):
     assert np.all(np.abs(freq - 10_000) < 3 * (100_000 * 0.09) ** 0.5)
 
 
+@pytest.fixture(params=["push", "pull"])
+def exchange(request, monkeypatch):
+    """Both data movements of the shuffle (md_shuffle_push / md_shuffle_pull)
+    place every byte identically."""
+    monkeypatch.setattr(dimd, "EXCHANGE", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("name", ["sh_a", "sh_b", "sh_c", "sh_d", "sh_e", "sh_f", "sh_g"])
-def test_shuffle_matches_reference(golden, name):
+def test_shuffle_matches_reference(golden, name, exchange):
     nrec, nr, gs, m, seed = (int(x) for x in golden[name + "_meta"])
     blob = golden[name + "_blob"].tobytes()
     entries = parse_index(golden[name + "_index"].tobytes())
@@ -83,7 +91,7 @@ def test_shuffle_matches_reference(golden, name):
     assert np.array_equal(np.concatenate([r[1] for r in res]), golden[name + "_labels"])
 
 
-def test_shuffle_all_equals_shuffle_group(golden):
+def test_shuffle_all_equals_shuffle_group(golden, exchange):
     blob = golden["sh_b_blob"].tobytes()
     entries = parse_index(golden["sh_b_index"].tobytes())
 
@@ -130,7 +138,7 @@ def test_index_parity_non_power_of_two_group(oracle):
             assert np.array_equal(fm.cpu().numpy(), wm) and np.array_equal(fr.cpu().numpy(), wr)
 
 
-def test_exchange_moves_every_byte(oracle):
+def test_exchange_moves_every_byte(oracle, exchange):
     """8 emulated ranks x 20,000 synthetic 4 KiB records: after the P2P
     shuffle every record is intact, in the reference's order, none lost."""
     n_local, L, seed, S = 20_000, 4096, 4242, 8

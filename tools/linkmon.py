@@ -31,12 +31,16 @@ class LinkMonitor:
         self.s0 = nv.nvmlGpmSampleAlloc()
         self.s1 = nv.nvmlGpmSampleAlloc()
         self.t0 = 0.0
+        nv.nvmlGpmSampleGet(self.h, self.s0)  # fails where GPM is not accessible
+
+    last_error = None
 
     @classmethod
     def create(cls, index: int):
         try:
             return cls(index)
-        except Exception:  # noqa: BLE001  (no NVML / no GPM: the caller reports null)
+        except Exception as e:  # noqa: BLE001  (no NVML / no GPM: the caller reports why)
+            cls.last_error = repr(e)
             return None
 
     def start(self):

@@ -55,6 +55,7 @@ def main() -> None:
     ap.add_argument("--per-graph", type=int, default=100)
     ap.add_argument("--max-skew-us", type=float, default=40.0)
     ap.add_argument("--sharded", action="store_true")
+    ap.add_argument("--route", default="auto", help="pin md_allreduce's kernel (tree, stream, ...)")
     a = ap.parse_args()
     ep = init_from_env()
     N, rank, dev = ep.n_ranks, ep.rank, ep.torch_device
@@ -96,7 +97,7 @@ def main() -> None:
             if cycles[i_static % a.per_graph] > 0:
                 torch.cuda._sleep(int(cycles[i_static % a.per_graph]))
             _lib.check(lib.md_fill_rank_input(grad.data.data_ptr(), L, rank, N, sptr))
-            allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False)
+            allreduce(ep, grad, "multicolor", tree_set=ts, update=upd, check=False, route=a.route)
             _lib.check(lib.md_sgd_update(w_ref.data_ptr(), g_ref.data_ptr(), m_ref.data_ptr(), P,
                                          c, MU, wd_b, sptr))
             idx = slot
