@@ -67,10 +67,11 @@ def args_():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the timed steps eagerly")
-    ap.add_argument("--update", choices=["replicated", "sharded"], default="replicated",
-                    help="SGD update mode of the fused call (SgdUpdate.sharded): every rank "
-                         "updates its replica, or the owner of each slice updates it and pushes "
-                         "the new weights (same bits)")
+    ap.add_argument("--update", choices=["replicated", "sharded"], default="sharded",
+                    help="SGD update mode of the fused call (SgdUpdate.sharded): the owner of "
+                         "each slice updates it and pushes the new weights (default; same "
+                         "weights bit for bit, momentum sharded), or every rank updates its "
+                         "full replica. Identical at N=1.")
     ap.add_argument("--nvlink-reps", type=int, default=40,
                     help="replays of the allreduce graph inside the NVLink-counter window")
     return ap.parse_args()
@@ -453,6 +454,7 @@ def run_ours(a) -> None:
             "k_colors": ts.k if ts else 1, "arity": ts.arity if ts else None,
             "parallelism": f"dp{N}",
             "cuda_graph": not a.no_graph,
+            "sgd_update": (a.update if N > 1 else "replicated (N=1)"),
             "input_pipeline": "batch i+1 drawn + gathered on a side stream (double-buffered slots) during step i",
             "l2": "inputs larger than L2 (W + momentum + gradient = 307 MB per GPU)",
         },

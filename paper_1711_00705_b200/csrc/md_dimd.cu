@@ -597,23 +597,41 @@ __global__ void __launch_bounds__(512) gather_kernel(const uint8_t* blob, const 
                                                      const uint64_t* out_off, uint32_t* out_label,
                                                      int32_t* bad, int chunks) {
   // work unit = (record, chunk of kGatherChunk bytes): a 32-record batch of
-  // 150 KB images spreads over ~150 CTAs instead of 32
+  // 150 KB images spreads over ~150 CTAs instead of 32. The next unit's
+  // metadata (picks -> off/len, two dependent loads) is fetched while the
+  // current chunk streams, so the chain's latency is off the copy's path.
   const int64_t units = batch * chunks;
-  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+  const int64_t G = gridDim.x;
+  int64_t u = blockIdx.x;
+  int64_t r = u < units ? picks[u / chunks] : 0;
+  uint32_t L = u < units ? len[r] : 0;
+  uint64_t o = u < units ? off[r] : 0;
+  int64_t r_next = u + G < units ? picks[(u + G) / chunks] : 0;
+  for (; u < units; u += G) {
+    uint32_t L_next = 0;
+    uint64_t o_next = 0;
+    if (u + G < units) {
+      L_next = len[r_next];
+      o_next = off[r_next];
+    }
+    const int64_t r_after = u + 2 * G < units ? picks[(u + 2 * G) / chunks] : 0;
     const int64_t b = u / chunks;
     const int c = static_cast<int>(u % chunks);
-    int64_t r = picks[b];
-    uint32_t L = len[r];
     if (stride > 0 && static_cast<int64_t>(L) != stride) {
       if (threadIdx.x == 0 && bad && c == 0) atomicExch(bad, 1);
-      continue;
+    } else {
+      uint8_t* dst = stride > 0 ? out + b * stride : out + out_off[b];
+      const uint64_t lo = chunks == 1 ? 0 : static_cast<uint64_t>(c) * kGatherChunk;
+      if (lo < L) {
+        const uint64_t n = chunks == 1 ? L : min(static_cast<uint64_t>(kGatherChunk), L - lo);
+        cta_copy(dst + lo, blob + o + lo, n);
+        if (threadIdx.x == 0 && c == 0 && out_label) out_label[b] = label[r];
+      }
     }
-    uint8_t* dst = stride > 0 ? out + b * stride : out + out_off[b];
-    const uint64_t lo = chunks == 1 ? 0 : static_cast<uint64_t>(c) * kGatherChunk;
-    if (lo >= L) continue;
-    const uint64_t n = chunks == 1 ? L : min(static_cast<uint64_t>(kGatherChunk), L - lo);
-    cta_copy(dst + lo, blob + off[r] + lo, n);
-    if (threadIdx.x == 0 && c == 0 && out_label) out_label[b] = label[r];
+    r = r_next;
+    L = L_next;
+    o = o_next;
+    r_next = r_after;
   }
 }
 

@@ -521,16 +521,20 @@ class _ShardArena:
                                   device=device)
         return slot[0][: max(1, nbytes)]
 
+    SENDLIST_HEAD = 1024  # begin[S + 1] first, at the same offset on every rank
+
     def sendlist(self, slot: list, n_final: int, S: int, device):
-        """The receiver's send list (24-byte entries, md_shuffle_sendlist) and
-        its begin[S + 1] array, in one peer-registrable allocation per slot."""
-        need = 24 * max(1, n_final) + 8 * (S + 1)
+        """The receiver's begin[S + 1] array and send list (24-byte entries,
+        md_shuffle_sendlist) in one peer-registrable allocation per slot:
+        begin at offset 0 and the list at SENDLIST_HEAD, so a peer finds both
+        from the base address whatever this rank's record count."""
+        need = self.SENDLIST_HEAD + 24 * max(1, n_final)
         if slot[3] is None or slot[3].numel() < need:
             slot[3] = None
             slot[3] = torch.empty(int(need * self.HEADROOM) + 64, dtype=torch.uint8,
                                   device=device)
         raw = slot[3]
-        return raw, raw[: 24 * max(1, n_final)], raw[24 * max(1, n_final): need].view(torch.int64)
+        return raw, raw[self.SENDLIST_HEAD: need], raw[: 8 * (S + 1)].view(torch.int64)
 
     @staticmethod
     def bind(slot: list, store) -> None:
@@ -634,8 +638,8 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
         torch.cuda.current_stream(dev).synchronize()  # lists complete before peers read them
         (v_out, v_list), _ = ep.register_varlen_many([blob, raw])
         mark("sendlist")
-        lst_ptrs = [v_list.ptrs[m] for m in members]
-        beg_ptrs = [p + (begin.data_ptr() - raw.data_ptr()) for p in lst_ptrs]
+        beg_ptrs = [v_list.ptrs[m] for m in members]
+        lst_ptrs = [p + _ShardArena.SENDLIST_HEAD for p in beg_ptrs]
         _lib.check(lib.md_shuffle_push(
             S, store.rank_in_group, store.blob.data_ptr(),
             (store.off if not empty else arrays[1]).data_ptr(),
