@@ -11,25 +11,26 @@
 //     every rank in ascending rank order. All three are one kernel here; the
 //     fold tree is data (md_plan_t).
 //
-// B200 design: ONE persistent kernel per call and rank. CTAs pull work items
-// (task, segment) from a per-rank queue ordered (segment, pipeline stage);
-// an UP item loads the children's segments straight out of the peers' HBM
-// over NVLink (16-byte vector loads, all children's loads in flight), folds
-// them in registers in the reference's order with __fadd_rn (no FMA), stores
-// the subtree sum in place, and releases a per-(color, segment) flag in the
-// parent's control block; a DOWN item copies the parent's final segment. The
-// optional prologue folds per-worker gradient buffers (sgd.py:335-353) into
-// the own value on the fly, and the optional epilogue applies the SGD
-// (momentum / weight-decay) update to the replicated weights as soon as a
-// segment's sum is final, so the gradient is never re-read from HBM.
+// B200 design: ONE persistent kernel per call and rank, picked per call
+// (md_allreduce_ex; md_plan_set_route pins one): LL push, one-shot pull,
+// owner-push (plain calls and the sharded SGD update), the tiled all-pull
+// stream kernel, the channelized tree and the work-queue tree. The tree
+// kernels move each color's chunk along its tree (UP folds in the reference
+// order with __fadd_rn, DOWN copies the parent's final); the others evaluate
+// each color's fold program (the same adds in the same order) on data pulled
+// or pushed over NVLink. The optional prologue folds per-worker gradient
+// buffers (sgd.py:335-353) into the own value, and the optional epilogue
+// applies the SGD (momentum / weight-decay) update as soon as a segment's
+// sum is final, so the gradient is never re-read from HBM.
 //
 // Synchronisation (replaces the transport's expose/pull and the length-header
 // barrier of _check_same_length, :157-174): epoch-tagged flags in peer-mapped
-// control blocks, written with st.release.sys after __threadfence_system and
-// polled with ld.acquire.sys; an entry barrier carries every rank's buffer
-// length (LengthMismatch) and an exit barrier guarantees no peer still reads
-// a buffer when the call returns. Waits are bounded by a globaltimer watchdog
-// (NotExposed). No flag is ever reset: epochs only grow.
+// control blocks, polled with ld.acquire.sys (published as described at
+// publish_flags); an entry barrier carries every rank's
+// buffer length (LengthMismatch) and route word (InvalidConfig) and an exit
+// barrier guarantees no peer still reads a buffer when the call returns.
+// Waits are bounded by a globaltimer watchdog (NotExposed). No flag is ever
+// reset: epochs only grow.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -383,9 +384,11 @@ __device__ __forceinline__ typename Elem<kVec>::T own_value(const AllreduceArgs&
 constexpr int kStages = 4;
 constexpr uint32_t kStageBytes = 48 * 1024;
 constexpr uint32_t kRingBytes = kStages * kStageBytes;
-// the stream kernel's ring: (almost) all of the 227 KB a CTA may opt into, so
-// N = 2 fused calls fit two stages of 7168-float tiles (4 slots: 2 ranks, W,
-// momentum); its static SMEM is ~1.4 KB
+// the stream and owner-push kernels' ring: (almost) all of the 227 KB a CTA
+// may opt into (their static SMEM is ~1.4 KB). The stream kernel's N = 2
+// fused calls fit two stages of <= 6656-float tiles (4 slots: 2 ranks, W,
+// momentum); the owner-push kernel's sharded calls 3-4 stages of [N ranks |
+// sum | W | momentum] at its ~2000-3000-float tiles
 constexpr uint32_t kStreamRingBytes = 224 * 1024;
 
 template <int kEpi>
