@@ -2678,7 +2678,11 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
       while ((B0 - A0 + TE - 1) / TE > kMaxTiles) TE *= 2;
       const int ups = epi == 0 ? 0 : (epi >= 3 ? 2 : 1);
       const int64_t stage_bytes = static_cast<int64_t>(N + 1 + ups) * TE * 4;
-      const int S = static_cast<int>(std::min<int64_t>(8, kStreamRingBytes / stage_bytes));
+      // ring: the 192 KB of round 1 for plain calls (measured: a 6th stage from
+      // the 224 KB ring made 1 GiB at N = 2 3 % slower), 224 KB when the W /
+      // momentum rows ride along (sharded update)
+      const int64_t ring = epi == 0 ? kRingBytes : kStreamRingBytes;
+      const int S = static_cast<int>(std::min<int64_t>(8, ring / stage_bytes));
       if (S >= 2) {
         const int64_t T = std::max<int64_t>(1, (B0 - A0 + TE - 1) / TE);
         const int g = static_cast<int>(std::min<int64_t>(avail, T));
