@@ -431,6 +431,8 @@ def run_ours(a) -> None:
                 "algorithmic_bytes_per_launch": algo_bytes, "kernel": kernel,
                 "route": {"name": route[0], "tile": route[1], "sharded": route[2]}}
     roof["traffic"], roof["traffic_source"] = _ncu_traffic(N, route)
+    if N > 1:  # the link-side counterpart: NVLink bytes per launch from ncu
+        roof["nvlink_traffic"] = _ncu_nvlink(N, route, ar_ms)
     line = {
         "metric": METRIC,
         "value": value,
@@ -495,6 +497,27 @@ def _ncu_traffic(n: int, route):
     if not rec:
         return None, None
     return rec["bytes"], rec["source"]
+
+
+def _ncu_nvlink(n: int, route, ar_ms: float):
+    """nvlrx/nvltx bytes per launch of the kernel that ran, from the committed
+    capture of rank 0 inside a live N-rank job (tools/ncu_rank0.sh,
+    profiles/nvlink_ncu.json), and the link rate they imply at this run's
+    allreduce time: user data (= the algorithmic bus bytes when nothing is
+    re-sent) and total link bytes incl. packet headers."""
+    f = ROOT / "profiles" / "nvlink_ncu.json"
+    try:
+        rec = json.loads(f.read_text()).get(f"{n}:{route[0]}:{int(route[2])}")
+    except Exception:  # noqa: BLE001
+        rec = None
+    if not rec:
+        return None
+    t = ar_ms / 1e3
+    return {"rx_user_bytes": rec["rx_user_bytes"], "rx_total_bytes": rec["rx_total_bytes"],
+            "tx_user_bytes": rec["tx_user_bytes"], "tx_total_bytes": rec["tx_total_bytes"],
+            "rx_user_gbps_at_this_run": rec["rx_user_bytes"] / t / 1e9,
+            "rx_total_gbps_at_this_run": rec["rx_total_bytes"] / t / 1e9,
+            "link_raw_peak_gbps": 18 * 53.125, "kernel": rec["kernel"], "source": rec["source"]}
 
 
 def _link_summary(rows, n: int, ar_ms: float):
