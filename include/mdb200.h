@@ -158,8 +158,8 @@ int md_last_route(int32_t device, int32_t* route, int64_t* tile, int32_t* sharde
  *                folds locally -- one NVLink trip, no barrier (MD_AR_LL_MAX);
  *   one-shot     N = 2 up to one SMEM pass of every rank's data (~14 MB):
  *                pull every peer buffer, fold locally (MD_AR_ONESHOT_MAX);
- *   owner-push   plain buffers (no fused update / worker fold) from 32 MiB at
- *                N = 2, 2 MiB above, and every SHARDED update
+ *   owner-push   plain buffers (no fused update / worker fold) from 4 MiB at
+ *                N = 2, 1 MiB above, and every SHARDED update
  *                (md_allreduce_ex): rank j pulls slice j of every rank,
  *                folds it with each element's color program and TMA-stores
  *                the result (or, sharded, the updated weights) into every

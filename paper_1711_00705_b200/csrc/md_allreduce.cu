@@ -2404,11 +2404,12 @@ const ArEnv& ar_env() {
 }
 
 // Smallest plain buffer (bytes) the owner-push kernel takes by default.
-// Measured against the tree (graph-timed sweep, profiles/README.md): N = 2
-// faster from 64 MiB (117 vs 127 us; 1 GiB 662 vs 645 GB/s bus) but slower at
-// 16 MiB; N = 4 faster from 4 MiB (31.6 vs 34.6 us) to 1 GiB (622 vs 601),
-// within 2 % at 256 MiB.
-int64_t push_min_bytes(int N) { return N == 2 ? (int64_t(32) << 20) : (int64_t(2) << 20); }
+// Measured against every other route (graph-timed C2 sweep, round 2,
+// profiles/r02_sweep_n{2,4}.csv): N = 2 push 22.3 us at 4 MiB (one-shot 23.0)
+// and 42.0 us at 16 MiB (tree 45.9-61.6), LL stays faster at 1 MiB (10.4 vs
+// 17.9); N = 4 push 19.3 us at 1 MiB (LL 20.6-20.9) and faster at every size
+// above.
+int64_t push_min_bytes(int N) { return N == 2 ? (int64_t(4) << 20) : (int64_t(1) << 20); }
 
 // Pipeline segment cap for a color chunk of `chunk` elements: about two
 // segments per SM, never below 4096 elements (the per-segment flag cost).
