@@ -350,17 +350,22 @@ def run_ours(a) -> None:
             out_tail = torch.empty(2, dtype=torch.float32).pin_memory()
             out_lab = torch.empty(BATCH, dtype=torch.int32).pin_memory()
             grads = [grad, GradientBuffer.alloc(P + 2, ep)]
-            copy_stream = torch.cuda.Stream(device=dev)
-            h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+            # the H2D as 4 chunks on 4 streams: several copy engines feed the
+            # PCIe link (tools/h2d_split_probe.py: 49.1 -> 54.4 GB/s)
+            copy_streams = [torch.cuda.Stream(device=dev) for _ in range(4)]
+            per = (P + 2 + 3) // 4
+            h2d_done = [[torch.cuda.Event() for _ in copy_streams] for _ in range(2)]
             buf_free = [torch.cuda.Event(), torch.cuda.Event()]
             for e in buf_free:
                 e.record(stream)
 
             def issue_h2d(i):
-                with torch.cuda.stream(copy_stream):
-                    copy_stream.wait_event(buf_free[i % 2])  # step i-2 finished with it
-                    grads[i % 2].data.copy_(host, non_blocking=True)  # H2D
-                    h2d_done[i % 2].record(copy_stream)
+                for j, cs in enumerate(copy_streams):
+                    with torch.cuda.stream(cs):
+                        cs.wait_event(buf_free[i % 2])  # step i-2 finished with it
+                        lo, hi = j * per, min(P + 2, (j + 1) * per)
+                        grads[i % 2].data[lo:hi].copy_(host[lo:hi], non_blocking=True)  # H2D
+                        h2d_done[i % 2][j].record(cs)
 
             def e2e_run(first, count):
                 issue_h2d(0)
@@ -368,7 +373,8 @@ def run_ours(a) -> None:
                 for i in range(count):
                     if i + 1 < count:
                         issue_h2d(i + 1)
-                    stream.wait_event(h2d_done[i % 2])
+                    for e in h2d_done[i % 2]:
+                        stream.wait_event(e)
                     key = dimd._mix64(SEED, SAMPLE_ROLE, rank, first + i)
                     random_batch_device(store, BatchRequest(BATCH, key), REC, slots)
                     g = grads[i % 2]

@@ -619,7 +619,7 @@ __device__ __forceinline__ void item_dispatch(const AllreduceArgs& a, const View
 // ---- optional tracing: %globaltimer events, producer and consumer halves ----
 constexpr int kTraceHalf = 512;  // events per CTA per role
 enum : uint16_t { EV_WAIT0 = 1, EV_WAIT1, EV_ISSUED, EV_FIRST, EV_DONE, EV_PUB, EV_ENTRY, EV_EXIT,
-                  EV_START, EV_LEFT, EV_X1, EV_X2 };
+                  EV_START, EV_LEFT, EV_X1, EV_X2, EV_X3 };
 
 __device__ __forceinline__ void trace_ev(const AllreduceArgs& a, int role, int& n, uint16_t ev,
                                          int seg) {
@@ -695,7 +695,7 @@ __device__ void exit_barrier(const AllreduceArgs& a, const ViewArgs& v, uint32_t
   if (!s_last) return;
   // last CTA of this rank: nobody here reads peer memory any more
   const int tid = threadIdx.x;
-  int tn = kTraceHalf - 6;
+  int tn = kTraceHalf - 8;  // (the channels kernel logs its own events in the last 4 slots)
   if (tid == 0) trace_ev(a, 0, tn, EV_X1, 0);
   if (tid < a.n_ranks && tid != v.rank) {
     if (a.flag_gpu_fence) {
@@ -721,6 +721,7 @@ __device__ void exit_barrier(const AllreduceArgs& a, const ViewArgs& v, uint32_t
         __nanosleep(32);
       }
     }
+    trace_ev(a, 0, tn, EV_X3, 0);  // every peer's done flag seen
     v.ctrl->queue_head = 0;
     v.ctrl->finished = 0;
     v.ctrl->abort_flag = 0;
@@ -1800,7 +1801,10 @@ __global__ void __launch_bounds__(kArThreads, 1)
   }
   __syncthreads();
   const uint32_t epoch = s_epoch;
+  int tn = 0;  // trace events (role 0: thread 0, role 1: storer, role 2: fold warp 0)
+  if (tid == 0) trace_ev(a, 0, tn, EV_START, 0);
   const bool ok = entry_barrier(a, v, local_cta, epoch);
+  if (tid == 0) trace_ev(a, 0, tn, EV_ENTRY, 0);
   if (ok) [&]() {
     if (tid < 32) {  // ---------------- producer (+ the buffer's tail) ----------------
       if (tid != 0) return;
@@ -1840,11 +1844,13 @@ __global__ void __launch_bounds__(kArThreads, 1)
     } else if (tid < kPushConsumerBase) {  // ---------------- storer ----------------
       if (tid != 32) return;
       uint32_t seq = 0;
+      int sn = 0;
       for (int64_t t = local_cta; t < T; t += G, ++seq) {
         const uint32_t st = seq % S;
         uint32_t spins = 0;
         while (!mbar_try_wait(&folded[st], (seq / S) & 1))
           if ((++spins & 1023) == 0 && aborted(v)) return;
+        if (seq == 0) trace_ev(a, 1, sn, EV_FIRST, 0);
         const int64_t lo = A + t * TE, hi = min(B, lo + TE);
         const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
         const float* stage = ringf + st * stage_f;
@@ -1880,7 +1886,9 @@ __global__ void __launch_bounds__(kArThreads, 1)
                        : "memory");
         }
       }
+      trace_ev(a, 1, sn, EV_ISSUED, static_cast<int>(seq));
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // every push has landed
+      trace_ev(a, 1, sn, EV_DONE, static_cast<int>(seq));
     } else {  // ---------------- fold (+ the slice's SGD update) ----------------
       const int ct = tid - kPushConsumerBase, nct = kPushConsumerWarps * 32;
       uint32_t seq = 0;
@@ -2443,6 +2451,23 @@ int64_t ll_max_bytes(int N) {
   return N <= 4 ? (int64_t(1) << 20) : (int64_t(256) << 10);
 }
 
+// diagnostics (MD_AR_TRACE=1): the per-CTA event log of this call, one per device
+int setup_trace(AllreduceArgs* a, int dev, int ctas, int n_views) {
+  a->trace = nullptr;
+  if (!ar_env().trace || dev < 0 || dev >= 64) return MD_OK;
+  const size_t bytes = sizeof(TraceEv) * 3 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
+  if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
+    if (g_trace[dev].ptr) cudaFree(g_trace[dev].ptr);
+    MD_CUDA_TRY(cudaMalloc(&g_trace[dev].ptr, bytes));
+    MD_CUDA_TRY(cudaMemset(g_trace[dev].ptr, 0, bytes));
+    g_trace[dev].bytes = bytes;
+  }
+  // (md_trace_dump re-zeroes the log, so a traced call adds no work of its own)
+  g_trace[dev].used = bytes;
+  a->trace = static_cast<TraceEv*>(g_trace[dev].ptr);
+  return MD_OK;
+}
+
 // cudaFuncSetAttribute(max dynamic SMEM) once per (kernel, device)
 int smem_attr_once(const void* k, int dev, size_t bytes) {
   static std::mutex mu;
@@ -2695,6 +2720,7 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
         const void* k = allreduce_push_kernel_of(epi);
         const size_t smem = static_cast<size_t>(S) * stage_bytes;
         int rc = smem_attr_once(k, dev, kStreamRingBytes);
+        if (rc == MD_OK) rc = setup_trace(&a, dev, g, n_views);
         if (rc == MD_OK) rc = launch_views(k, g, n_views, smem, &a, stream);
         if (rc == MD_OK) record_route(dev, MD_ROUTE_PUSH, TE, shard_ok);
         return rc;
@@ -2845,20 +2871,8 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
   a.max_stage = max_stage;
   // the queue and channelized kernels exchange the same per-segment flags
   a.cfg_word = cfg_word_of(MD_ROUTE_TREE, owner, false, a.seg);
-  a.trace = nullptr;
-  if (env.trace) {  // diagnostics: one event log per device, per call
-    const size_t bytes = sizeof(TraceEv) * 3 * kTraceHalf * static_cast<size_t>(ctas) * n_views;
-    if (!g_trace[dev].ptr || g_trace[dev].bytes < bytes) {
-      if (g_trace[dev].ptr) cudaFree(g_trace[dev].ptr);
-      MD_CUDA_TRY(cudaMalloc(&g_trace[dev].ptr, bytes));
-      MD_CUDA_TRY(cudaMemset(g_trace[dev].ptr, 0, bytes));
-      g_trace[dev].bytes = bytes;
-    }
-    // (md_trace_dump re-zeroes the log, so a traced call adds no work of its own)
-    g_trace[dev].used = bytes;
-    a.trace = static_cast<TraceEv*>(g_trace[dev].ptr);
-  }
-  rc = launch_views(kern, ctas, n_views, kRingBytes, &a, stream);
+  rc = setup_trace(&a, dev, ctas, n_views);
+  if (rc == MD_OK) rc = launch_views(kern, ctas, n_views, kRingBytes, &a, stream);
   if (rc == MD_OK) record_route(dev, chan ? MD_ROUTE_TREE : MD_ROUTE_QUEUE, a.seg, false);
   return rc;
 }

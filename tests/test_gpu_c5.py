@@ -156,3 +156,55 @@ def test_c5_sharded_two_gpus(oracle):
     ts = build_multicolor_trees(2, 2, 4)
     res = run_ranks(2, "cuda", _prog(arrays, w0, c, wd_b, ts, 2, True), emulate=False).results
     _check(res, 2, g, want_w, want_m, True, "push")
+
+
+@pytest.mark.parametrize("n,L,ulen,algo", [
+    (2, 4099, 4096, "multicolor"),      # update covers all but the unaligned tail
+    (4, 100_003, 50_000, "multicolor"),  # half the buffer past the update range
+    (4, 100_004, 0, "multicolor"),      # empty update range: a plain push
+    (3, 65_537, 32_768, "ring"),        # ring fold programs, odd world size
+    (8, 200_002, 199_996, "reduce_bcast"),
+])
+def test_sharded_update_edges(oracle, n, L, ulen, algo):
+    """Sharded update where the update range ends inside the push slices: W'
+    is pushed for [0, ulen), the plain sum for [ulen, n) -- on every rank --
+    and each rank's own slice of the sum and of the momentum is exact."""
+    from paper_1711_00705_b200.topology import build_ring
+
+    rng = np.random.default_rng(n * 1000 + L)
+    arrays = [rng.standard_normal(L).astype(np.float32) for _ in range(n)]
+    w0 = rng.standard_normal(max(ulen, 1)).astype(np.float32)
+    m0 = rng.standard_normal(max(ulen, 1)).astype(np.float32)
+    if algo == "multicolor":
+        tables = oracle.tables_from_trees(n, oracle.trees(n, min(n, 4), 4))
+        kw = {"tree_set": build_multicolor_trees(n, min(n, 4), 4)}
+    elif algo == "ring":
+        tables = oracle.ring_tables(list(range(n)))
+        kw = {"ring": build_ring(n)}
+    else:
+        tables = oracle.star_tables(n, 0)
+        kw = {"root": 0}
+    g = oracle.fold_c(tables, arrays)
+
+    def prog(ep):
+        dev = ep.torch_device
+        w, _ = ep.alloc(max(ulen, 1))
+        w.copy_(torch.from_numpy(w0))
+        m = torch.from_numpy(m0.copy()).to(dev)
+        buf = GradientBuffer(torch.from_numpy(arrays[ep.rank]).to(dev))
+        allreduce(ep, buf, algo, update=SgdUpdate(weights=w, c=1e-3, momentum=m, mu=MU,
+                                                  wd_b=3.2e-3, update_len=ulen, sharded=True),
+                  **kw)
+        return buf.data.cpu().numpy(), w.cpu().numpy(), m.cpu().numpy(), _lib.last_route(ep.device)
+
+    res = run_ranks(n, "cuda", prog, emulate=True).results
+    want_w, want_m = oracle.sgd_np(w0[:ulen], g[:ulen], m0[:ulen].copy(), 1e-3, MU, 3.2e-3)
+    for r, (gb, w, m, route) in enumerate(res):
+        assert route[0] == "push" and route[2], route
+        assert np.array_equal(w[:ulen], want_w), f"rank {r}: weights"
+        assert np.array_equal(gb[ulen:], g[ulen:]), f"rank {r}: sum past the update range"
+        lo, hi = _push_slice(L, n, r)
+        assert np.array_equal(gb[lo:hi], g[lo:hi]), f"rank {r}: own slice of the sum"
+        a, b = lo, min(hi, ulen)
+        if b > a:
+            assert np.array_equal(m[a:b], want_m[a:b]), f"rank {r}: own momentum"
