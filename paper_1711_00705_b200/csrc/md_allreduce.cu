@@ -641,8 +641,7 @@ __device__ bool entry_barrier(const AllreduceArgs& a, const ViewArgs& v, int loc
     Ctrl* pc = v.peer_ctrl[tid];
     st_relaxed_sys64(reinterpret_cast<uint64_t*>(&pc->arrive_len[v.rank]), mylen);
     st_relaxed_sys64(reinterpret_cast<uint64_t*>(&pc->arrive_cfg[v.rank]), a.cfg_word);
-    __threadfence_system();
-    st_release_sys(&pc->arrive_epoch[v.rank], epoch);
+    st_release_sys(&pc->arrive_epoch[v.rank], epoch);  // (release: orders both words first)
   }
   __shared__ int s_ok;
   if (tid == 0) {
@@ -1762,6 +1761,23 @@ __host__ __device__ __forceinline__ void push_slice(int64_t n, int N, int j, int
   *hi = h < n4 ? h : n4;
 }
 
+// Tile t of an owner slice [A, A + L): the first `nsmall` tiles (one per CTA)
+// are a quarter of the full size, so every CTA's first fold -- and with it
+// the first pushes -- needs a quarter of the bytes (the pipeline ramp keeps the
+// push direction of the links idle until then).
+struct PushTiles {
+  int64_t A, L, TE, TEs, nsmall, T;
+  __device__ PushTiles(int64_t a, int64_t b, int64_t te, int ctas) : A(a), L(b - a), TE(te) {
+    TEs = max(int64_t(4), (te / 4) & ~int64_t(3));
+    nsmall = min(static_cast<int64_t>(ctas), L / TEs);
+    T = nsmall + (L - nsmall * TEs + TE - 1) / TE;
+  }
+  __device__ void span(int64_t t, int64_t* lo, int64_t* hi) const {
+    *lo = t < nsmall ? A + t * TEs : A + nsmall * TEs + (t - nsmall) * TE;
+    *hi = min(A + L, *lo + (t < nsmall ? TEs : TE));
+  }
+};
+
 template <int kEpi>
 __global__ void __launch_bounds__(kArThreads, 1)
     allreduce_push_kernel(const __grid_constant__ AllreduceArgs a) {
@@ -1769,7 +1785,6 @@ __global__ void __launch_bounds__(kArThreads, 1)
   constexpr bool kMom = kEpi >= 3;
   const int view = blockIdx.x / a.ctas_per_view;
   const int local_cta = blockIdx.x % a.ctas_per_view;
-  const int G = a.ctas_per_view;
   const ViewArgs& v = a.v[view];
   const int tid = threadIdx.x;
   const int N = a.n_ranks, me = v.rank;
@@ -1777,7 +1792,8 @@ __global__ void __launch_bounds__(kArThreads, 1)
   const int S = a.lag;
   int64_t A, B;
   push_slice(a.n, N, me, &A, &B);
-  const int64_t T = (B - A + TE - 1) / TE;
+  const PushTiles tiles(A, B, TE, a.ctas_per_view);
+  const int64_t T = tiles.T;
   const int64_t ulen = kUpd ? a.update_len : 0;  // a multiple of 4 (host)
   const size_t slot_f = static_cast<size_t>(TE);
   const int w_slot = N + 1, m_slot = N + 2;
@@ -1785,6 +1801,7 @@ __global__ void __launch_bounds__(kArThreads, 1)
   const size_t stage_f = slot_f * (N + 1 + (kUpd ? (kMom ? 2 : 1) : 0));
   __shared__ uint32_t s_epoch;
   __shared__ __align__(8) uint64_t full[8], empty[8], folded[8];
+  __shared__ int64_t s_tile[8];  // the tile a stage holds (-1: no more work)
   __shared__ FoldProg prog;
   extern __shared__ __align__(128) char ring[];
   float* ringf = reinterpret_cast<float*>(ring);
@@ -1820,15 +1837,27 @@ __global__ void __launch_bounds__(kArThreads, 1)
         __threadfence_system();  // tail pushes are generic stores: visible before our done flag
       }
       fence_proxy_async_global();
-      uint32_t seq = 0;
-      for (int64_t t = local_cta; t < T; t += G, ++seq) {
+      // tiles are handed out dynamically (a per-call counter in the own
+      // control block, reset by the exit barrier): CTAs whose NVLink traffic
+      // is served faster take more tiles, so all of them finish together
+      // (static round-robin tiles measured a 115-240 us spread of CTA finish
+      // times at N = 4, profiles/r02_trace_n4_sharded.json)
+      for (uint32_t seq = 0;; ++seq) {
         const uint32_t st = seq % S;
         if (seq >= static_cast<uint32_t>(S)) {
           uint32_t spins = 0;
           while (!mbar_try_wait(&empty[st], ((seq / S) - 1) & 1))
             if ((++spins & 1023) == 0 && aborted(v)) return;
         }
-        const int64_t lo = A + t * TE, hi = min(B, lo + TE);
+        const int64_t t = atomicAdd(&v.ctrl->queue_head, 1u);
+        if (t >= T) {  // no more work: a sentinel stage ends the consumers and the storer
+          s_tile[st] = -1;
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&full[st])) : "memory");
+          return;
+        }
+        s_tile[st] = t;
+        int64_t lo, hi;
+        tiles.span(t, &lo, &hi);
         const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
         const int64_t whi = min(hi, ulen);
         const uint32_t wbytes = whi > lo ? static_cast<uint32_t>((whi - lo) * 4) : 0u;
@@ -1845,13 +1874,16 @@ __global__ void __launch_bounds__(kArThreads, 1)
       if (tid != 32) return;
       uint32_t seq = 0;
       int sn = 0;
-      for (int64_t t = local_cta; t < T; t += G, ++seq) {
+      for (;; ++seq) {
         const uint32_t st = seq % S;
         uint32_t spins = 0;
         while (!mbar_try_wait(&folded[st], (seq / S) & 1))
           if ((++spins & 1023) == 0 && aborted(v)) return;
+        const int64_t t = s_tile[st];
+        if (t < 0) break;
         if (seq == 0) trace_ev(a, 1, sn, EV_FIRST, 0);
-        const int64_t lo = A + t * TE, hi = min(B, lo + TE);
+        int64_t lo, hi;
+        tiles.span(t, &lo, &hi);
         const uint32_t bytes = static_cast<uint32_t>((hi - lo) * 4);
         const float* stage = ringf + st * stage_f;
         const float* res = stage + N * slot_f;
@@ -1891,15 +1923,23 @@ __global__ void __launch_bounds__(kArThreads, 1)
       trace_ev(a, 1, sn, EV_DONE, static_cast<int>(seq));
     } else {  // ---------------- fold (+ the slice's SGD update) ----------------
       const int ct = tid - kPushConsumerBase, nct = kPushConsumerWarps * 32;
-      uint32_t seq = 0;
-      for (int64_t t = local_cta; t < T; t += G, ++seq) {
+      for (uint32_t seq = 0;; ++seq) {
         const uint32_t st = seq % S;
         uint32_t spins = 0;
         while (!mbar_try_wait(&full[st], (seq / S) & 1))
           if ((++spins & 1023) == 0 && aborted(v)) return;
+        const int64_t t = s_tile[st];
+        if (t < 0) {  // pass the sentinel on to the storer
+          __syncwarp();
+          if ((ct & 31) == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&folded[st])) : "memory");
+          return;
+        }
         float* stage = ringf + st * stage_f;
         float* res = stage + N * slot_f;
-        const int64_t lo = A + t * TE, len = min(B, lo + TE) - lo;
+        int64_t lo, hi;
+        tiles.span(t, &lo, &hi);
+        const int64_t len = hi - lo;
         const int64_t wlen = kUpd ? max(int64_t(0), min(len, ulen - lo)) : 0;
         for (int64_t e = 4 * ct; e < len; e += 4 * nct) {
           const int c0 = color_of(a.n, a.k, lo + e);
