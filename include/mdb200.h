@@ -261,11 +261,14 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
  * (segment, source member, source order) and the final local permutation
  * Philox(_mix64(seed,"perm",global_rank)).permutation(N') are applied, and
  * final_member/final_rec name the source record of every output slot.
- * n_rec: host array of S record counts. cap >= sum(n_rec). */
+ * n_rec: host array of S record counts. cap >= sum(n_rec).
+ * next_counts (host array of S, nullable) receives every member's record
+ * count AFTER this shuffle -- the next epoch's n_rec, identical on every
+ * member (each one draws every source's destinations). */
 int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
                     uint64_t global_rank, int64_t m_segments, const int64_t* n_rec,
                     int32_t* final_member, int64_t* final_rec, int64_t cap, int64_t* n_final,
-                    void* stream);
+                    int64_t* next_counts, void* stream);
 
 /* Build the new shard index from the sources' (peer-mapped) index arrays:
  * lengths/labels in final order and offsets by exclusive prefix sum

@@ -91,7 +91,7 @@ SIGNATURES = {
     "md_shuffle_plan": (
         C.c_int,
         [_u64, _u64, _i32, _i32, _u64, _i64, C.POINTER(_i64), _vp, _vp, _i64, C.POINTER(_i64),
-         _vp],
+         C.POINTER(_i64), _vp],
     ),
     "md_shuffle_index": (
         C.c_int, [_i32, _pp, _pp, _vp, _vp, _i64, _vp, _vp, _vp, C.POINTER(_u64), _vp]

@@ -219,6 +219,22 @@ __global__ void mine_flag_kernel(const int32_t* dest, int64_t total, int32_t me,
   if (g < total) flag[g] = dest[g] == me;
 }
 
+// records per destination member: every member's record count after this
+// shuffle (the next shuffle's n_rec, so it can start its plan before the
+// counts' host collective returns)
+__global__ void dest_count_kernel(const int32_t* dest, int64_t total, int32_t S,
+                                  unsigned long long* cnt) {
+  __shared__ unsigned int h[MD_MAX_GROUP];
+  for (int q = threadIdx.x; q < S; q += blockDim.x) h[q] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&h[dest[i]], 1u);
+  __syncthreads();
+  for (int q = threadIdx.x; q < S; q += blockDim.x)
+    if (h[q]) atomicAdd(&cnt[q], static_cast<unsigned long long>(h[q]));
+}
+
 // receive-order bases: base[t][q] in (t-major, q) order -- dimd.py:303-335
 __global__ void recv_base_kernel(const __grid_constant__ SrcTable tab, int32_t S, int64_t m,
                                  const int32_t* excl /* total+1 entries */, int64_t* base_tq,
@@ -867,7 +883,7 @@ struct PlanTimer {
 int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
                     uint64_t global_rank, int64_t m_segments, const int64_t* n_rec,
                     int32_t* final_member, int64_t* final_rec, int64_t cap, int64_t* n_final,
-                    void* stream) {
+                    int64_t* next_counts, void* stream) {
   if (S < 1 || S > MD_MAX_GROUP || member < 0 || member >= S) {
     set_error("bad group shape S=%d member=%d (max group %d)", S, member, MD_MAX_GROUP);
     return MD_ERR_INVALID_CONFIG;
@@ -907,6 +923,7 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
 
   int32_t *dest = nullptr, *flag = nullptr, *excl = nullptr, *got_m = nullptr;
   int64_t *got_r = nullptr, *base_tq = nullptr, *d_nf = nullptr;
+  unsigned long long* d_cnt = nullptr;
   uint8_t* seg_bad = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
@@ -917,6 +934,8 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
   MD_CUDA_TRY(cudaMallocAsync(&seg_bad, S * m, s));
   MD_CUDA_TRY(cudaMallocAsync(&base_tq, sizeof(int64_t) * S * m, s));
   MD_CUDA_TRY(cudaMallocAsync(&d_nf, sizeof(int64_t), s));
+  MD_CUDA_TRY(cudaMallocAsync(&d_cnt, sizeof(unsigned long long) * MD_MAX_GROUP, s));
+  MD_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * MD_MAX_GROUP, s));
   MD_CUDA_TRY(cudaMemsetAsync(seg_bad, 0, S * m, s));
   MD_CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int32_t) * tot1, s));
   if (total > 0) {
@@ -928,6 +947,10 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
     }
     mine_flag_kernel<<<blocks_for(total), 256, 0, s>>>(dest, total, member, flag);
     MD_LAUNCH_CHECK();
+    if (next_counts) {
+      dest_count_kernel<<<std::min(blocks_for(total), 1024), 256, 0, s>>>(dest, total, S, d_cnt);
+      MD_LAUNCH_CHECK();
+    }
   }
   pt.mark("dest draws");
   MD_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, excl, tot1, s));
@@ -937,8 +960,15 @@ int md_shuffle_plan(uint64_t seed, uint64_t group_id, int32_t S, int32_t member,
   recv_base_kernel<<<1, 1, 0, s>>>(tab, S, m, excl, base_tq, d_nf);
   MD_LAUNCH_CHECK();
   int64_t nf = 0;
+  unsigned long long cnt_h[MD_MAX_GROUP] = {0};
   MD_CUDA_TRY(cudaMemcpyAsync(&nf, d_nf, sizeof(nf), cudaMemcpyDeviceToHost, s));
+  if (next_counts)
+    MD_CUDA_TRY(cudaMemcpyAsync(cnt_h, d_cnt, sizeof(unsigned long long) * S,
+                                cudaMemcpyDeviceToHost, s));
+  MD_CUDA_TRY(cudaFreeAsync(d_cnt, s));
   MD_CUDA_TRY(cudaStreamSynchronize(s));
+  if (next_counts)
+    for (int q = 0; q < S; ++q) next_counts[q] = static_cast<int64_t>(cnt_h[q]);
   if (nf > cap) {
     set_error("shuffle output of %lld records exceeds capacity %lld", (long long)nf,
               (long long)cap);

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -597,25 +598,58 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
               torch.zeros(1, dtype=torch.int64, device=dev) if empty else store.off,
               torch.zeros(1, dtype=torch.int32, device=dev) if empty else store.length,
               torch.zeros(1, dtype=torch.int32, device=dev) if empty else store.label]
-    (v_blob, v_off, v_len, v_lab), rows = ep.register_varlen_many(
-        arrays, (int(store.n_records), int(m_segments)))
-    n_rec = _group_counts(rows, members, int(m_segments))
-    mark("register")
-    cap = max(1, sum(n_rec))
-    fm = torch.empty(cap, dtype=torch.int32, device=dev)
-    fr = torch.empty(cap, dtype=torch.int64, device=dev)
-    nf = C.c_int64()
     lib = _lib.load()
     s = _stream(dev)
-    n_rec_arr = (C.c_int64 * S)(*n_rec)
-    _lib.check(
-        lib.md_shuffle_plan(
+
+    def plan(n_rec):
+        cap = max(1, sum(n_rec))
+        fm = torch.empty(cap, dtype=torch.int32, device=dev)
+        fr = torch.empty(cap, dtype=torch.int64, device=dev)
+        nf = C.c_int64()
+        nxt = (C.c_int64 * S)()
+        _lib.check(lib.md_shuffle_plan(
             seed & _MASK64, store.group_id, S, store.rank_in_group, ep.rank, int(m_segments),
-            n_rec_arr, fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), s,
-        )
-    )
-    mark("plan")
-    n_final = int(nf.value)
+            (C.c_int64 * S)(*n_rec), fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), nxt, s))
+        return fm, fr, int(nf.value), [int(x) for x in nxt]
+
+    meta = (int(store.n_records), int(m_segments))
+    pred = getattr(store, "_next_counts", None)
+    if pred is not None and (len(pred) != S or pred[store.rank_in_group] != store.n_records):
+        pred = None
+    if pred is None:
+        (v_blob, v_off, v_len, v_lab), rows = ep.register_varlen_many(arrays, meta)
+        n_rec = _group_counts(rows, members, int(m_segments))
+        mark("register")
+        fm, fr, n_final, next_counts = plan(n_rec)
+        mark("plan")
+    else:
+        # the previous shuffle's plan already counted every member's records
+        # (md_shuffle_plan next_counts): plan on this thread (the C call drops
+        # the GIL) while the host collective runs on a helper thread, then check
+        # the prediction against the gathered counts
+        box: dict = {}
+
+        def register():
+            try:
+                torch.cuda.set_device(dev)  # IPC imports map into the current device
+                box["r"] = ep.register_varlen_many(arrays, meta)
+            except BaseException as e:  # noqa: BLE001  (re-raised on the caller's thread)
+                box["e"] = e
+
+        th = threading.Thread(target=register, daemon=True)
+        th.start()
+        try:
+            planned = plan(pred)
+        finally:
+            th.join()
+        if "e" in box:
+            raise box["e"]
+        (v_blob, v_off, v_len, v_lab), rows = box["r"]
+        n_rec = _group_counts(rows, members, int(m_segments))
+        if n_rec != pred:
+            planned = plan(n_rec)
+        fm, fr, n_final, next_counts = planned
+        mark("register+plan")
     arena = _arena(ep)
     (off, ln, lb), slot = arena.take(n_final, dev)
     total = C.c_uint64()
@@ -662,6 +696,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     out = ShardStore(blob, off[:n_final], ln[:n_final], lb[:n_final], store.group_id, S,
                      store.rank_in_group)
     out._nbytes = int(total.value)
+    out._next_counts = next_counts  # lets the next shuffle plan while its counts travel
     _ShardArena.bind(slot, out)
     return out
 
@@ -680,7 +715,7 @@ def shuffle_plan_device(seed: int, group_id: int, S: int, member: int, global_ra
     _lib.check(
         _lib.load().md_shuffle_plan(
             seed & _MASK64, group_id, S, member, global_rank, int(m_segments), arr,
-            fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), _stream(device),
+            fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), None, _stream(device),
         )
     )
     return fm[: nf.value], fr[: nf.value]

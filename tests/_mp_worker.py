@@ -76,8 +76,8 @@ def main() -> None:
             out[f"shuffle{epoch}_bytes"] = int(bad) == 0
             out[f"shuffle{epoch}_count"] = new.n_records == len(mem)
             store = new
-            if epoch == 0:
-                out["shuffle0_indices"] = bool(np.array_equal(gids.cpu().numpy(), mem + N * rec))
+            # epoch 1 plans from the counts epoch 0 predicted (dimd._shuffle)
+            out[f"shuffle{epoch}_indices"] = bool(np.array_equal(gids.cpu().numpy(), mem + N * rec))
         # 4. every allreduce kernel under CUDA-graph replay (device epochs,
         #    LL inbox parity, read-done / arrival flags): 3 captured calls, each
         #    on a refilled buffer, replayed twice; bitwise vs the oracle fold

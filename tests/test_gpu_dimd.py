@@ -272,3 +272,31 @@ def test_batch_stream_with_rejections(oracle):
     assert hit >= 3  # the rejection path really ran
     assert int(bs.step.item()) == 140
     bs.slots.check()
+
+
+@pytest.mark.parametrize("corrupt_prediction", [False, True])
+def test_successive_shuffles_plan_from_predicted_counts(oracle, exchange, corrupt_prediction):
+    """From the second epoch on, a shuffle plans with the record counts the
+    previous plan predicted (md_shuffle_plan next_counts) while the counts'
+    host collective runs; a wrong prediction is caught and re-planned. Every
+    epoch's slots are checked against the oracle's plan with the true counts."""
+    S, n_local, L, seed = 4, 3_000, 64, 31
+
+    def prog(ep):
+        st = dimd.synth_store(n_local, L, ep.rank, S, seed, 0, S, ep.rank, device=ep.torch_device)
+        ok = []
+        for epoch in range(3):
+            counts = ep.all_gather(st.n_records)
+            if epoch and corrupt_prediction:
+                st._next_counts = [c + 1 for c in counts]
+            elif epoch:
+                ok.append(st._next_counts == counts)
+            key = oracle.mix64(seed, oracle.SHUF_ROLE, epoch)
+            st = shuffle_all(ep, st, m_segments=3, seed=key)
+            bad, gids = dimd.synth_verify(st, seed)
+            mem, rec = oracle.shuffle_plan_c(key, 0, S, ep.rank, ep.rank, 3, counts)
+            ok.append(bad == 0 and np.array_equal(gids.cpu().numpy(), mem + S * rec))
+        return ok
+
+    for r in run_ranks(S, "cuda", prog, emulate=True).results:
+        assert all(r), r
