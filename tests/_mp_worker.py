@@ -65,6 +65,7 @@ def main() -> None:
         #    vs the generator (shard arrays mapped through IPC)
         n = 3000
         store = dimd.synth_store(n, 256, rank, N, 11, 0, N, rank, device=dev)
+        held = ep.all_gather(np.arange(n, dtype=np.int64) * N + rank)  # gid per (member, index)
         for epoch in range(2):
             key = O.mix64(11, O.SHUF_ROLE, epoch)
             counts = ep.all_gather(store.n_records)
@@ -77,7 +78,10 @@ def main() -> None:
             out[f"shuffle{epoch}_count"] = new.n_records == len(mem)
             store = new
             # epoch 1 plans from the counts epoch 0 predicted (dimd._shuffle)
-            out[f"shuffle{epoch}_indices"] = bool(np.array_equal(gids.cpu().numpy(), mem + N * rec))
+            got = gids.cpu().numpy().astype(np.int64)
+            want = np.array([held[q][r] for q, r in zip(mem, rec)], dtype=np.int64)
+            out[f"shuffle{epoch}_indices"] = bool(np.array_equal(got, want))
+            held = ep.all_gather(got)
         # 4. every allreduce kernel under CUDA-graph replay (device epochs,
         #    LL inbox parity, read-done / arrival flags): 3 captured calls, each
         #    on a refilled buffer, replayed twice; bitwise vs the oracle fold

@@ -285,6 +285,8 @@ def test_successive_shuffles_plan_from_predicted_counts(oracle, exchange, corrup
     def prog(ep):
         st = dimd.synth_store(n_local, L, ep.rank, S, seed, 0, S, ep.rank, device=ep.torch_device)
         ok = []
+        # global record id held by (member, local index) before each epoch
+        held = ep.all_gather(np.arange(n_local, dtype=np.int64) * S + ep.rank)
         for epoch in range(3):
             counts = ep.all_gather(st.n_records)
             if epoch and corrupt_prediction:
@@ -295,7 +297,10 @@ def test_successive_shuffles_plan_from_predicted_counts(oracle, exchange, corrup
             st = shuffle_all(ep, st, m_segments=3, seed=key)
             bad, gids = dimd.synth_verify(st, seed)
             mem, rec = oracle.shuffle_plan_c(key, 0, S, ep.rank, ep.rank, 3, counts)
-            ok.append(bad == 0 and np.array_equal(gids.cpu().numpy(), mem + S * rec))
+            want = np.array([held[m][r] for m, r in zip(mem, rec)], dtype=np.int64)
+            got = gids.cpu().numpy().astype(np.int64)
+            ok.append(bad == 0 and np.array_equal(got, want))
+            held = ep.all_gather(got)
         return ok
 
     for r in run_ranks(S, "cuda", prog, emulate=True).results:
