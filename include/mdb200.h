@@ -156,8 +156,9 @@ int md_last_route(int32_t device, int32_t* route, int64_t* tile, int32_t* sharde
  *   LL push      n*4 <= 1 MiB (N <= 4; 256 KiB above): every rank pushes
  *                (value, epoch) words into its peers' control-block inbox and
  *                folds locally -- one NVLink trip, no barrier (MD_AR_LL_MAX);
- *   one-shot     N = 2 up to one SMEM pass of every rank's data (~14 MB):
- *                pull every peer buffer, fold locally (MD_AR_ONESHOT_MAX);
+ *   one-shot     N = 2 between the LL and owner-push ranges (up to one SMEM
+ *                pass of every rank's data, ~14 MB, when pinned): pull every
+ *                peer buffer, fold locally (MD_AR_ONESHOT_MAX);
  *   owner-push   plain buffers (no fused update / worker fold) from 4 MiB at
  *                N = 2, 1 MiB above, and every SHARDED update
  *                (md_allreduce_ex): rank j pulls slice j of every rank,
