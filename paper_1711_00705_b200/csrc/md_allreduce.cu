@@ -149,6 +149,7 @@ struct AllreduceArgs {
   const FoldProg* prog;    // every color's fold program (one-shot / LL / stream / owner)
   int32_t prog_k;          // colors of the fold programs (the plan's k; a.k counts owner slices)
   int32_t sharded;         // push kernel: sharded SGD update (W' pushed, momentum sharded)
+  int32_t exit_sys_release;  // done flags certify REMOTE writes (owner-push): release at sys scope
   // route word every rank publishes at the entry barrier: ranks that picked a
   // different kernel / tile / segment / schedule / update mode fail together
   // with InvalidConfig instead of exchanging differently-shaped flags
@@ -697,10 +698,13 @@ __device__ void exit_barrier(const AllreduceArgs& a, const ViewArgs& v, uint32_t
   int tn = kTraceHalf - 8;  // (the channels kernel logs its own events in the last 4 slots)
   if (tid == 0) trace_ev(a, 0, tn, EV_X1, 0);
   if (tid < a.n_ranks && tid != v.rank) {
-    if (a.flag_gpu_fence) {
+    if (a.flag_gpu_fence && !a.exit_sys_release) {
       st_relaxed_sys(&v.peer_ctrl[tid]->done_epoch[v.rank], epoch);
     } else {
-      __threadfence_system();
+      // owner-push: the flag also certifies our bulk stores INTO the peer
+      // (complete per wait_group 0 in every CTA, ordered by the acq_rel CTA
+      // counter); a system-scope release makes that formal, once per call
+      if (!a.flag_gpu_fence) __threadfence_system();
       st_release_sys(&v.peer_ctrl[tid]->done_epoch[v.rank], epoch);
     }
   }
@@ -2756,6 +2760,7 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
         a.lag = S;
         a.ctas_per_view = g;
         a.sharded = shard_ok;
+        a.exit_sys_release = 1;
         a.cfg_word = cfg_word_of(MD_ROUTE_PUSH, false, shard_ok, TE);
         const void* k = allreduce_push_kernel_of(epi);
         const size_t smem = static_cast<size_t>(S) * stage_bytes;
