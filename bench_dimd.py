@@ -51,6 +51,8 @@ def main() -> None:
     ap.add_argument("--epochs", type=int, default=5)
     ap.add_argument("--exchange", choices=["push", "pull"], default="push",
                     help="shuffle data movement (dimd.EXCHANGE)")
+    ap.add_argument("--no-prefetch-plan", dest="prefetch_plan", action="store_false",
+                    help="do not pass next_seed (plan every epoch inside its own shuffle)")
     ap.add_argument("--cpu-records", type=int, default=1024,
                     help="records per member of the host (CPU reference) shuffle row; 0 = none")
     a = ap.parse_args()
@@ -80,7 +82,8 @@ def main() -> None:
             t0 = time.perf_counter()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(ep.stream)
-            out = dimd.shuffle_all(ep, store, m_segments=m_seg, seed=key)
+            nxt = O.mix64(a.seed, O.SHUF_ROLE, epoch + 1) if a.prefetch_plan else None
+            out = dimd.shuffle_all(ep, store, m_segments=m_seg, seed=key, next_seed=nxt)
             e1.record(ep.stream)
             torch.cuda.synchronize(dev)
             walls.append(time.perf_counter() - t0)
@@ -165,6 +168,7 @@ def main() -> None:
             "batch32_is": "BatchStream.next() (picks + gather), 100 per CUDA graph, device time",
             "batch32_records_per_s_per_gpu": 32 / (max(r[5] for r in rows) / 1e3),
             "exchange": a.exchange,
+            "plan_prefetch": a.prefetch_plan,
             "bulk_gather_records": a.bulk,
             "bulk_gather_is": "random_batch_device: Philox picks of --bulk records + gather kernel",
             "bulk_gather_ms": max(r[8] for r in rows),

@@ -770,6 +770,17 @@ static int blocks_for(int64_t n, int t = 256) {
   return static_cast<int>(b < 1 ? 1 : (b > (1LL << 30) ? (1LL << 30) : b));
 }
 
+// The shuffle's exchange kernels: 2 CTAs x 512 threads per SM keep the links
+// saturated (each CTA has 32 KB of 16-byte loads in flight) and leave every SM
+// room for the next epoch's plan kernels on a side stream (shuffle_all's
+// next_seed).
+static int exchange_grid(int64_t n) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int64_t cap = static_cast<int64_t>(sm_count(dev)) * 2;
+  return static_cast<int>(n < 1 ? 1 : (n < cap ? n : cap));
+}
+
 static int record_grid(int64_t n) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1135,7 +1146,7 @@ int md_shuffle_pull(int32_t S, const uint8_t* const* peer_blob, const uint64_t* 
     p.blob[q] = peer_blob[q];
     p.off[q] = peer_off[q];
   }
-  pull_kernel<<<record_grid(n_final), 512, 0, as_stream(stream)>>>(
+  pull_kernel<<<exchange_grid(n_final), 512, 0, as_stream(stream)>>>(
       p, final_member, final_rec, n_final, out_off, out_len, out_blob);
   MD_LAUNCH_CHECK();
   return MD_OK;
@@ -1203,9 +1214,8 @@ int md_shuffle_push(int32_t S, int32_t member, const uint8_t* blob, const uint64
     p.begin[d] = peer_begin[d];
     p.out[d] = peer_out[d];
   }
-  int dev = 0;
-  MD_CUDA_TRY(cudaGetDevice(&dev));
-  push_kernel<<<sm_count(dev) * 4, 512, 0, as_stream(stream)>>>(p, S, member, blob, off);
+  push_kernel<<<exchange_grid(int64_t(1) << 30), 512, 0, as_stream(stream)>>>(p, S, member, blob,
+                                                                             off);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }

@@ -440,17 +440,25 @@ def _check_group(ep, store: ShardStore) -> None:
         )
 
 
-def shuffle_all(ep, store: ShardStore, m_segments: int | None = None, seed: int = 0) -> ShardStore:
-    """Exchange records within each group, all ranks participating (dimd.py:261-269)."""
+def shuffle_all(ep, store: ShardStore, m_segments: int | None = None, seed: int = 0, *,
+                next_seed: int | None = None) -> ShardStore:
+    """Exchange records within each group, all ranks participating (dimd.py:261-269).
+
+    ``next_seed`` (extension, optional): the next epoch's shuffle key. The
+    next epoch's plan is then computed on a side stream while this epoch's
+    records cross the links, and the returned store carries it; the next
+    ``shuffle_all`` with that key (and the same record counts) skips its plan.
+    The bits never depend on it."""
     _check_group(ep, store)
-    return _shuffle(ep, store, m_segments, seed)
+    return _shuffle(ep, store, m_segments, seed, next_seed)
 
 
-def shuffle_group(ep, store: ShardStore, m_segments: int | None = None, seed: int = 0) -> ShardStore:
+def shuffle_group(ep, store: ShardStore, m_segments: int | None = None, seed: int = 0, *,
+                  next_seed: int | None = None) -> ShardStore:
     """Exchange inside this rank's group (dimd.py:272-278). Keys do not depend
     on the communicator layout, so the result equals ``shuffle_all``'s."""
     _check_group(ep, store)
-    return _shuffle(ep, store, m_segments, seed)
+    return _shuffle(ep, store, m_segments, seed, next_seed)
 
 
 def group_record_counts(channel, members, n_records: int, m_segments: int) -> list[int]:
@@ -575,7 +583,16 @@ class _PhaseClock:
         self.t = now
 
 
-def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
+def _side_stream(ep) -> torch.cuda.Stream:
+    st = getattr(ep, "_dimd_side_stream", None)
+    if st is None:
+        st = torch.cuda.Stream(device=ep.torch_device)
+        ep._dimd_side_stream = st
+    return st
+
+
+def _shuffle(ep, store: ShardStore, m_segments, seed: int, next_seed: int | None = None
+             ) -> ShardStore:
     S = store.group_size
     if S > _lib.MD_MAX_GROUP:
         raise InvalidConfig(f"group size {S} exceeds {_lib.MD_MAX_GROUP}")
@@ -601,22 +618,35 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
     lib = _lib.load()
     s = _stream(dev)
 
-    def plan(n_rec):
+    def plan(n_rec, key=seed, stream=s):
         cap = max(1, sum(n_rec))
         fm = torch.empty(cap, dtype=torch.int32, device=dev)
         fr = torch.empty(cap, dtype=torch.int64, device=dev)
         nf = C.c_int64()
         nxt = (C.c_int64 * S)()
         _lib.check(lib.md_shuffle_plan(
-            seed & _MASK64, store.group_id, S, store.rank_in_group, ep.rank, int(m_segments),
-            (C.c_int64 * S)(*n_rec), fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), nxt, s))
+            key & _MASK64, store.group_id, S, store.rank_in_group, ep.rank, int(m_segments),
+            (C.c_int64 * S)(*n_rec), fm.data_ptr(), fr.data_ptr(), cap, C.byref(nf), nxt, stream))
         return fm, fr, int(nf.value), [int(x) for x in nxt]
 
+    def plan_key(key):
+        return (key & _MASK64, store.group_id, S, store.rank_in_group, ep.rank, int(m_segments))
+
     meta = (int(store.n_records), int(m_segments))
+    pre = getattr(store, "_prefetched", None)  # (key, counts, plan) from the previous epoch
     pred = getattr(store, "_next_counts", None)
     if pred is not None and (len(pred) != S or pred[store.rank_in_group] != store.n_records):
         pred = None
-    if pred is None:
+    if pre is not None and pre[0] == plan_key(seed):
+        # planned during the previous exchange (next_seed): only the counts'
+        # collective remains, and a changed count re-plans
+        (v_blob, v_off, v_len, v_lab), rows = ep.register_varlen_many(arrays, meta)
+        n_rec = _group_counts(rows, members, int(m_segments))
+        fm, fr, n_final, next_counts = pre[2] if n_rec == pre[1] else plan(n_rec)
+        for t in (fm, fr):  # allocated on the side stream, used on this one
+            t.record_stream(torch.cuda.current_stream(dev))
+        mark("register (plan prefetched)")
+    elif pred is None:
         (v_blob, v_off, v_len, v_lab), rows = ep.register_varlen_many(arrays, meta)
         n_rec = _group_counts(rows, members, int(m_segments))
         mark("register")
@@ -687,8 +717,30 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
                 n_final, off.data_ptr(), ln.data_ptr(), blob.data_ptr(), s,
             )
         )
+    prefetched = None
+    if next_seed is not None:
+        # the next epoch's plan, on a side stream while the bytes move (the
+        # exchange kernel leaves room on every SM for the plan's kernels)
+        side = _side_stream(ep)
+        box: dict = {}
+
+        def prefetch():
+            try:
+                torch.cuda.set_device(dev)
+                with torch.cuda.stream(side):
+                    box["p"] = plan(next_counts, next_seed, _lib.stream_ptr(side))
+                side.synchronize()
+            except BaseException as e:  # noqa: BLE001  (no prefetch: the next epoch plans)
+                box["e"] = e
+
+        th = threading.Thread(target=prefetch, daemon=True)
+        th.start()
     torch.cuda.current_stream(dev).synchronize()
     mark(EXCHANGE)
+    if next_seed is not None:
+        th.join()
+        if "p" in box:
+            prefetched = (plan_key(next_seed), next_counts, box["p"])
     # pull: every read of our old shard is done before anyone frees it;
     # push: every record pushed into our new blob has landed
     ep.barrier()
@@ -697,6 +749,7 @@ def _shuffle(ep, store: ShardStore, m_segments, seed: int) -> ShardStore:
                      store.rank_in_group)
     out._nbytes = int(total.value)
     out._next_counts = next_counts  # lets the next shuffle plan while its counts travel
+    out._prefetched = prefetched
     _ShardArena.bind(slot, out)
     return out
 

@@ -351,7 +351,10 @@ def run_training(
             gstep = 0
             for epoch in range(cfg.epochs):
                 if cfg.shuffle_every > 0 and epoch % cfg.shuffle_every == 0:
-                    store = shuffle_all(ep, store, seed=_mix64(cfg.seed, SHUFFLE_ROLE, epoch))
+                    nxt = epoch + cfg.shuffle_every  # the next reshuffle's key: plan it early
+                    store = shuffle_all(ep, store, seed=_mix64(cfg.seed, SHUFFLE_ROLE, epoch),
+                                        next_seed=(_mix64(cfg.seed, SHUFFLE_ROLE, nxt)
+                                                   if nxt < cfg.epochs else None))
                 t0 = time.perf_counter()
                 loss_sum, correct = 0.0, 0
                 for _ in range(steps_per_epoch):

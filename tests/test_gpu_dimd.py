@@ -274,12 +274,16 @@ def test_batch_stream_with_rejections(oracle):
     bs.slots.check()
 
 
+@pytest.mark.parametrize("prefetch", [False, True])
 @pytest.mark.parametrize("corrupt_prediction", [False, True])
-def test_successive_shuffles_plan_from_predicted_counts(oracle, exchange, corrupt_prediction):
+def test_successive_shuffles_plan_from_predicted_counts(oracle, exchange, corrupt_prediction,
+                                                       prefetch):
     """From the second epoch on, a shuffle plans with the record counts the
     previous plan predicted (md_shuffle_plan next_counts) while the counts'
-    host collective runs; a wrong prediction is caught and re-planned. Every
-    epoch's slots are checked against the oracle's plan with the true counts."""
+    host collective runs; a wrong prediction is caught and re-planned. With
+    ``next_seed`` the next epoch's whole plan is computed during this epoch's
+    exchange (and recomputed when the counts changed). Every epoch's slots are
+    checked against the oracle's plan with the true counts."""
     S, n_local, L, seed = 4, 3_000, 64, 31
 
     def prog(ep):
@@ -291,10 +295,15 @@ def test_successive_shuffles_plan_from_predicted_counts(oracle, exchange, corrup
             counts = ep.all_gather(st.n_records)
             if epoch and corrupt_prediction:
                 st._next_counts = [c + 1 for c in counts]
+                if st._prefetched is not None:
+                    pk, pc, pp = st._prefetched
+                    st._prefetched = (pk, [c + 1 for c in pc], pp)
             elif epoch:
                 ok.append(st._next_counts == counts)
+                ok.append((st._prefetched is not None) == prefetch)
             key = oracle.mix64(seed, oracle.SHUF_ROLE, epoch)
-            st = shuffle_all(ep, st, m_segments=3, seed=key)
+            nxt = oracle.mix64(seed, oracle.SHUF_ROLE, epoch + 1) if prefetch else None
+            st = shuffle_all(ep, st, m_segments=3, seed=key, next_seed=nxt)
             bad, gids = dimd.synth_verify(st, seed)
             mem, rec = oracle.shuffle_plan_c(key, 0, S, ep.rank, ep.rank, 3, counts)
             want = np.array([held[m][r] for m, r in zip(mem, rec)], dtype=np.int64)
