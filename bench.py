@@ -85,6 +85,20 @@ def hbm_peak() -> tuple[float, str]:
         return HBM_FALLBACK, "B200_PROFILING.md fallback"
 
 
+def workload_config(n: int) -> dict:
+    """The C5 workload both arms run (bench line `config`, identical for
+    `--impl ours` and `--impl reference`)."""
+    ts = tree_config(n)
+    return {
+        "workload": "C5: DIMD gather 32 rec/GPU + synthetic 25.6M-float gradient + fused "
+                    "multicolor allreduce + SGD(momentum 0.9, wd 1e-4), per step",
+        "global_batch": n * BATCH, "per_gpu_batch": BATCH, "record_bytes": REC,
+        "shard_records_per_gpu": SHARD, "params": P, "algo": "multicolor",
+        "k_colors": ts.k if ts else 1, "arity": ts.arity if ts else None,
+        "parallelism": f"dp{n}",
+    }
+
+
 def tree_config(n: int):
     """The reference's default plan (sgd.py:453-467 comm_plan): widest k."""
     from paper_1711_00705_b200.sgd import comm_plan
@@ -454,13 +468,8 @@ def run_ours(a) -> None:
         "dtype": "f32",
         "data": "synthetic (device-generated 224x224x3 uint8 records; deterministic fill "
                 "gradient; random-init weights)",
-        "config": {
-            "workload": "C5: DIMD gather 32 rec/GPU + synthetic 25.6M-float gradient + fused "
-                        "multicolor allreduce + SGD(momentum 0.9, wd 1e-4), per step",
-            "global_batch": N * BATCH, "per_gpu_batch": BATCH, "record_bytes": REC,
-            "shard_records_per_gpu": SHARD, "params": P, "algo": "multicolor",
-            "k_colors": ts.k if ts else 1, "arity": ts.arity if ts else None,
-            "parallelism": f"dp{N}",
+        "config": workload_config(N),
+        "execution": {
             "cuda_graph": not a.no_graph,
             "sgd_update": (a.update if N > 1 else "replicated (N=1)"),
             "input_pipeline": "batch i+1 drawn + gathered on a side stream (double-buffered slots) during step i",
@@ -668,8 +677,8 @@ def run_reference(a) -> None:
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": N,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": {"workload": "C5 (see bench.py docstring), CPU port",
-                                         "global_batch": N * BATCH, "parallelism": f"dp{N}"},
+        "data": "synthetic", "config": workload_config(N),
+        "execution": {"host": f"oracle/mdoracle.c C port of the step, {threads} threads"},
         "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
