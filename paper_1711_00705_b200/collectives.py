@@ -469,9 +469,11 @@ class VarPayload:
 def alltoallv(ep, send: VarPayload) -> VarPayload:
     """Personalized exchange; received slices ordered by source rank.
 
-    Lengths/offsets are gathered host-side (the reference's length round,
+    Lengths/offsets are gathered host-side together with the send buffers'
+    IPC handles (one collective; the reference's length round,
     collectives.py:485-494); the bytes are pulled by one kernel from every
-    source's registered send buffer (NVLink reads)."""
+    source's registered send buffer (NVLink reads); a final barrier keeps
+    every send buffer alive until its readers are done."""
     send.validate(ep.n_ranks)
     host = not isinstance(send.data, torch.Tensor)
     if host:
@@ -483,8 +485,10 @@ def alltoallv(ep, send: VarPayload) -> VarPayload:
     if src.numel() == 0:
         src = torch.zeros(1, dtype=torch.uint8, device=ep.torch_device)
     torch.cuda.current_stream(ep.torch_device).synchronize()
-    tables = ep.all_gather((tuple(send.offsets), tuple(send.lengths)))
-    view = ep.register_varlen(src)
+    # one host collective: every rank's slice table (the reference's length
+    # round, collectives.py:485-494) rides with its send buffer's IPC handle
+    (view,), tables = ep.register_varlen_many(
+        [src], (tuple(send.offsets), tuple(send.lengths)))
     me = ep.rank
     lens = [tables[s][1][me] for s in range(ep.n_ranks)]
     offs_out = np.concatenate([[0], np.cumsum(lens)])[:-1].astype(np.int64).tolist()
