@@ -15,8 +15,9 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmdb200.so"
-SOURCES = ["md_elementwise.cu", "md_allreduce.cu", "md_dimd.cu"]
-HEADERS = ["md_common.cuh", "../../include/mdb200.h"]
+SOURCES = ["md_elementwise.cu", "md_allreduce.cu", "md_ar_tree.cu", "md_ar_direct.cu", "md_ar_push.cu",
+           "md_dimd.cu"]
+HEADERS = ["md_common.cuh", "md_allreduce.cuh", "../../include/mdb200.h"]
 
 NVCC_FLAGS = [
     "-std=c++17",
