@@ -1,7 +1,7 @@
 """Allreduce (multi-color tree, ring, reduce+broadcast) and AllToAllV on B200.
 
 API of /root/reference/pkg/src/minidist/collectives.py, executed by
-libmdb200's persistent P2P kernel (csrc/md_allreduce.cu):
+libmdb200's persistent P2P kernels (csrc/md_ar_*.cu, routed by csrc/md_allreduce.cu):
 
 * ``allreduce_multicolor`` (:225-268), ``allreduce_ring`` (:302-359) and
   ``reduce_then_broadcast`` (:365-409) differ only in their fold tree

@@ -33,7 +33,7 @@ MU, WD, LR = 0.9, 1e-4, 0.1
 
 
 def _push_slice(n_elems: int, n: int, j: int) -> tuple[int, int]:
-    """md_allreduce.cu push_slice: 16-byte aligned owner slice j."""
+    """push_slice (csrc/md_allreduce.cuh): 16-byte aligned owner slice j."""
     n4 = n_elems & ~3
     per = ((n4 // 4 + n - 1) // n) * 4
     return min(n4, j * per), min(n4, (j + 1) * per)
