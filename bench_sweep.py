@@ -49,6 +49,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+C1_BYTES = 25_600_000 * 4  # BASELINE config C1: 25.6M floats
 CSV_HEADER = ("scenario,algorithm,n_ranks,payload_bytes,median_time_s,throughput_GBps,backend,"
               "route,cores")
 
@@ -87,7 +88,9 @@ def main() -> None:
     sizes = [4 << 10]
     while sizes[-1] * 4 <= a.max_mb << 20:
         sizes.append(sizes[-1] * 4)
-    max_elems = sizes[-1] // 4
+    if C1_BYTES <= a.max_mb << 20:  # the ResNet-50 gradient itself (C1 / C3 size)
+        sizes = sorted(set(sizes + [C1_BYTES]))
+    max_elems = max(sizes) // 4
     buf = GradientBuffer.alloc(max_elems, ep)  # one registered buffer, views per size
     plans = []
     for k in (1, 2, 4, 8):
@@ -214,8 +217,8 @@ def main() -> None:
 
     # the reference algorithm on the host CPU (rank 0; after the GPU rows)
     if rank == 0 and a.cpu_max_mb > 0 and N > 1:
-        rows.extend(cpu_rows(N, [x for x in sizes if x <= a.cpu_max_mb << 20], plans,
-                             a.cpu_seconds))
+        rows.extend(cpu_rows(N, [x for x in sizes if x <= a.cpu_max_mb << 20 or x == C1_BYTES],
+                             plans, a.cpu_seconds))
     ep.barrier()
 
     if rank == 0:
