@@ -25,6 +25,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 #include <vector>
 
@@ -1214,8 +1215,8 @@ int md_shuffle_push(int32_t S, int32_t member, const uint8_t* blob, const uint64
     p.begin[d] = peer_begin[d];
     p.out[d] = peer_out[d];
   }
-  push_kernel<<<exchange_grid(int64_t(1) << 30), 512, 0, as_stream(stream)>>>(p, S, member, blob,
-                                                                             off);
+  // (work items are records, many per CTA: the full exchange grid)
+  push_kernel<<<exchange_grid(INT64_MAX), 512, 0, as_stream(stream)>>>(p, S, member, blob, off);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
