@@ -208,3 +208,46 @@ def test_sharded_update_edges(oracle, n, L, ulen, algo):
         a, b = lo, min(hi, ulen)
         if b > a:
             assert np.array_equal(m[a:b], want_m[a:b]), f"rank {r}: own momentum"
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_sharded_update_random_shapes(oracle, seed):
+    """Random world sizes, color counts, buffer lengths (ragged tails) and
+    update ranges: the sharded owner-push update gives the oracle's weights
+    on every rank, and each rank's own slices of the sum and the momentum."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(2, 7))
+    ks = [k for k in (1, 2, 4, 8) if k <= n]
+    k = int(rng.choice(ks))
+    arity = 7 if k == 8 else 4
+    try:
+        ts = build_multicolor_trees(n, k, arity)
+    except Exception:  # noqa: BLE001  (unconstructible shape: fall back to one color)
+        k, ts = 1, build_multicolor_trees(n, 1, 4)
+    L = int(rng.integers(1_000, 400_000))
+    ulen = int(rng.integers(0, L + 1)) & ~3
+    arrays = [rng.standard_normal(L).astype(np.float32) for _ in range(n)]
+    w0 = rng.standard_normal(max(ulen, 1)).astype(np.float32)
+    m0 = rng.standard_normal(max(ulen, 1)).astype(np.float32)
+    g = oracle.fold_c(oracle.tables_from_trees(n, oracle.trees(n, k, arity if k > 1 else 4)),
+                      arrays)
+    want_w, want_m = oracle.sgd_np(w0[:ulen], g[:ulen], m0[:ulen].copy(), 1e-3, MU, 3.2e-3)
+
+    def prog(ep):
+        w, _ = ep.alloc(max(ulen, 1))
+        w.copy_(torch.from_numpy(w0))
+        m = torch.from_numpy(m0.copy()).to(ep.torch_device)
+        buf = GradientBuffer(torch.from_numpy(arrays[ep.rank]).to(ep.torch_device))
+        allreduce(ep, buf, "multicolor", tree_set=ts,
+                  update=SgdUpdate(weights=w, c=1e-3, momentum=m, mu=MU, wd_b=3.2e-3,
+                                   update_len=ulen, sharded=True))
+        return buf.data.cpu().numpy(), w.cpu().numpy(), m.cpu().numpy(), _lib.last_route(ep.device)
+
+    for r, (gb, w, m, route) in enumerate(run_ranks(n, "cuda", prog, emulate=True).results):
+        assert route[0] == "push" and route[2], (n, k, L, ulen, route)
+        assert np.array_equal(w[:ulen], want_w), (n, k, L, ulen, r)
+        assert np.array_equal(gb[ulen:], g[ulen:]), (n, k, L, ulen, r)
+        lo, hi = _push_slice(L, n, r)
+        assert np.array_equal(gb[lo:hi], g[lo:hi]), (n, k, L, ulen, r)
+        if min(hi, ulen) > lo:
+            assert np.array_equal(m[lo:min(hi, ulen)], want_m[lo:min(hi, ulen)])
