@@ -607,6 +607,12 @@ __global__ void __launch_bounds__(512) push_kernel(const __grid_constant__ PushA
 
 constexpr uint64_t kGatherChunk = 32 * 1024;
 
+// kStep: the variant for training-step batches, which runs between the
+// allreduce's 192-224 KB-SMEM kernels and therefore asks for the max-shared
+// carveout (no L1/SMEM re-partition); bulk gathers take the other variant with
+// the default carveout -- the max-shared one costs them 20 % (6.29 vs 5.03
+// TB/s, tools/gather_variants.cu)
+template <bool kStep>
 __global__ void __launch_bounds__(512) gather_kernel(const uint8_t* blob, const uint64_t* off,
                                                      const uint32_t* len, const uint32_t* label,
                                                      const int64_t* picks, int64_t batch,
@@ -782,10 +788,15 @@ static int exchange_grid(int64_t n) {
   return static_cast<int>(n < 1 ? 1 : (n < cap ? n : cap));
 }
 
+// Record-copy grids (gather, synthetic corpus): up to 8 CTAs of 512 threads
+// per SM, i.e. two waves of resident CTAs -- the second wave evens out the
+// per-CTA unit counts (tools/gather_variants.cu, 8,192 random 150 KB records:
+// 5.89 TB/s with 4 CTAs per SM, 6.39 TB/s with 8; cudaMemcpy of the same
+// bytes 6.49 TB/s).
 static int record_grid(int64_t n) {
   int dev = 0;
   cudaGetDevice(&dev);
-  int64_t cap = static_cast<int64_t>(sm_count(dev)) * 4;
+  int64_t cap = static_cast<int64_t>(sm_count(dev)) * 8;
   return static_cast<int>(n < 1 ? 1 : (n < cap ? n : cap));
 }
 
@@ -862,10 +873,18 @@ int md_gather(const uint8_t* blob, const uint64_t* off, const uint32_t* len, con
   }
   const int chunks =
       out_stride > 0 ? static_cast<int>((out_stride + kGatherChunk - 1) / kGatherChunk) : 1;
-  static std::atomic<uint64_t> carve{0};
-  prefer_max_smem(gather_kernel, carve);
-  gather_kernel<<<record_grid(batch * chunks), 512, 0, as_stream(stream)>>>(
-      blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
+  int dev = 0;
+  MD_CUDA_TRY(cudaGetDevice(&dev));
+  const int64_t units = batch * chunks;
+  if (units <= static_cast<int64_t>(sm_count(dev)) * 2) {  // a training-step batch
+    static std::atomic<uint64_t> carve{0};
+    prefer_max_smem(gather_kernel<true>, carve);
+    gather_kernel<true><<<record_grid(units), 512, 0, as_stream(stream)>>>(
+        blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
+  } else {
+    gather_kernel<false><<<record_grid(units), 512, 0, as_stream(stream)>>>(
+        blob, off, len, label, picks, batch, out, out_stride, out_off, out_label, err_flag, chunks);
+  }
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
