@@ -1234,8 +1234,11 @@ int md_shuffle_push(int32_t S, int32_t member, const uint8_t* blob, const uint64
     p.begin[d] = peer_begin[d];
     p.out[d] = peer_out[d];
   }
-  // (work items are records, many per CTA: the full exchange grid)
-  push_kernel<<<exchange_grid(INT64_MAX), 512, 0, as_stream(stream)>>>(p, S, member, blob, off);
+  // (work items are records, many per CTA: the full exchange grid; a
+  // one-member group only copies within its own HBM, where the record-copy
+  // grid's second wave of CTAs evens out the tail)
+  const int grid = S == 1 ? record_grid(INT64_MAX) : exchange_grid(INT64_MAX);
+  push_kernel<<<grid, 512, 0, as_stream(stream)>>>(p, S, member, blob, off);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
