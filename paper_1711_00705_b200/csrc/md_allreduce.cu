@@ -589,13 +589,13 @@ int smem_attr_once(const void* k, int dev, size_t bytes) {
 // wait on other GPUs (never on a sibling CTA), so a plain launch of <= one
 // CTA per SM is deadlock-free there.
 int launch_views(const void* k, unsigned grid, int n_views, size_t smem, AllreduceArgs* a,
-                 void* stream) {
+                 void* stream, int threads = kArThreads) {
   void* args[] = {a};
   if (n_views > 1) {
-    MD_CUDA_TRY(cudaLaunchCooperativeKernel(k, dim3(grid * n_views), dim3(kArThreads), args, smem,
+    MD_CUDA_TRY(cudaLaunchCooperativeKernel(k, dim3(grid * n_views), dim3(threads), args, smem,
                                             as_stream(stream)));
   } else {
-    MD_CUDA_TRY(cudaLaunchKernel(k, dim3(grid), dim3(kArThreads), args, smem, as_stream(stream)));
+    MD_CUDA_TRY(cudaLaunchKernel(k, dim3(grid), dim3(threads), args, smem, as_stream(stream)));
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return MD_OK;
@@ -938,7 +938,8 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
   int rc = smem_attr_once(kern, dev, kRingBytes);
   if (rc != MD_OK) return rc;
   int per_sm = 0;
-  MD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArThreads,
+  const int threads = chan ? kChanThreads : kArThreads;
+  MD_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads,
                                                              kRingBytes));
   const int resident = per_sm * sm_count(dev);
   if (ctas <= 0) ctas = resident / n_views;
@@ -959,7 +960,7 @@ int md_allreduce_ex(md_comm_t* const* comms, int32_t n_views, const md_plan_t* p
   // the queue and channelized kernels exchange the same per-segment flags
   a.cfg_word = cfg_word_of(MD_ROUTE_TREE, owner, false, a.seg);
   rc = setup_trace(&a, dev, ctas, n_views);
-  if (rc == MD_OK) rc = launch_views(kern, ctas, n_views, kRingBytes, &a, stream);
+  if (rc == MD_OK) rc = launch_views(kern, ctas, n_views, kRingBytes, &a, stream, threads);
   if (rc == MD_OK) record_route(dev, chan ? MD_ROUTE_TREE : MD_ROUTE_QUEUE, a.seg, false);
   return rc;
 }

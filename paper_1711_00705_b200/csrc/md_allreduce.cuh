@@ -55,6 +55,7 @@ constexpr int kMaxSegs = 4096;        // per color
 constexpr int kLLElems = 262144;      // LL inbox: payload floats per (parity, source)
 constexpr int kMaxTiles = 65536;      // stream kernel: tiles per call
 constexpr int kArThreads = 512;
+constexpr int kChanThreads = 384;  // channelized tree kernel (see md_ar_tree.cu)
 // float4 per thread per source per pass: 512 threads x 2 x 16 B keeps >= 16 KB
 // per SM in flight per source (NVLink needs ~5 KB/SM at 775 GB/s x 1 us)
 constexpr int kUnroll = 2;

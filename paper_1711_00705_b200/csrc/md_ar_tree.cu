@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kArThreads, 1)
 // overlap; segments can stay small (fine-grained pipelining across GPUs).
 // warp 0: TMA producer, warp 1: notifier (publishes finished segments, so the
 // flag fences never stall the consumers), warps 2..15: consumers
-constexpr int kConsumerWarps = kArThreads / 32 - 2;
+constexpr int kConsumerWarps = kChanThreads / 32 - 2;
 constexpr int kConsumerBase = 64;
 constexpr int kDoneSlots = 8;  // segments a notifier may lag behind the consumers
 
@@ -787,7 +787,7 @@ __device__ void run_channel(const AllreduceArgs& a, const ViewArgs& v, const Tas
 }
 
 template <int kEpi>
-__global__ void __launch_bounds__(kArThreads, 1)
+__global__ void __launch_bounds__(kChanThreads, 1)
     allreduce_channels_kernel(const __grid_constant__ AllreduceArgs a) {
   const int view = blockIdx.x / a.ctas_per_view;
   const int local_cta = blockIdx.x % a.ctas_per_view;
