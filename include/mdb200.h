@@ -328,6 +328,28 @@ int md_synth_verify(const uint8_t* blob, const uint64_t* off, const uint32_t* le
  * side (replaces host blake2b). *digest is written on the host. */
 int md_digest_f32(const float* x, int64_t n, uint64_t* digest, void* stream);
 
+/* ---- gradient producer: ToyModel.loss_and_grad_sum, sgd.py:220-248 ---------
+ * The reference's model (one-hidden-layer tanh MLP + softmax cross entropy,
+ * weights [W1 | b1 | W2 | b2] as one flat float32 vector of
+ * p = n_in*hidden + hidden + hidden*n_classes + n_classes) on every worker's
+ * sub-batch, writing node_gradient's buffer (sgd.py:335-353) per worker:
+ * out[j][0..p) = float32(summed gradient), out[j][p] = loss sum,
+ * out[j][p+1] = correct count. Float64 math in numpy's evaluation order,
+ * bit-identical to the reference's float32 outputs.
+ * records[j]: batch rows of record_stride bytes whose first
+ * feature_bytes*n_in bytes are little-endian features, float32 (feature_bytes
+ * 4: the DIMD records, sgd.py:310-313) or float64 (8: grad(), sgd.py:250-257);
+ * labels[j]: int32 class
+ * indices (negative ones wrap like numpy indices); records / labels / out are
+ * HOST arrays of n_workers DEVICE pointers. status (device, nullable) gets
+ * 1 + the first row whose label is out of range (the reference's IndexError).
+ * MD_ERR_LENGTH_MISMATCH if record_stride < feature_bytes*n_in; MD_ERR_INVALID_CONFIG if
+ * the batch does not fit one CTA's shared memory. */
+int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t n_classes,
+                const uint8_t* const* records, int32_t feature_bytes,
+                const int32_t* const* labels, int64_t record_stride, int32_t batch,
+                float* const* out, int32_t n_workers, int32_t* status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,6 +13,7 @@
  * pkg/pyproject.toml:11; the restatement is checked against numpy itself in
  * tests/test_oracle.py).
  */
+#include <math.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -360,4 +361,110 @@ int64_t mo_shuffle_plan(uint64_t seed, uint64_t group_id, int S, int member, uin
 /* random_batch picks, dimd.py:213-220 */
 void mo_random_batch(uint64_t key, int64_t n_records, int64_t batch, int64_t* picks) {
   mo_integers(key, (uint64_t)n_records, batch, picks);
+}
+
+/* ---- the reference's gradient producer: ToyModel.loss_and_grad_sum ---------
+ * sgd.py:148-248: one-hidden-layer tanh MLP + softmax cross entropy, all math
+ * in float64 from the float32 weights, gradient rounded to float32 once.
+ * numpy's float64 matmul (OpenBLAS dgemm) accumulates every output element
+ * over the inner index in order with fused multiply-adds (measured against
+ * numpy here for batch >= 2); row sums of exp are sequential (numpy's pairwise
+ * sum is sequential below 8 terms), column sums (axis 0) sequential over
+ * rows, the loss sum numpy's pairwise sum. Weights [W1 | b1 | W2 | b2]. */
+static double np_pairwise(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = -0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    int64_t i;
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+/* x: [k][n_in] float32 record values; y: labels; out: p + 2 floats
+ * (gradient sum, loss sum, correct count -- node_gradient's buffer, sgd.py:335-353) */
+void mo_toy_grad(const float* w, int n_in, int hidden, int ncls, const float* x,
+                 const int64_t* y, int k, float* out) {
+  const int o_b1 = n_in * hidden, o_w2 = o_b1 + hidden, o_b2 = o_w2 + hidden * ncls;
+  const int p = o_b2 + ncls;
+  double* h = (double*)malloc(sizeof(double) * (size_t)k * hidden);
+  double* pr = (double*)malloc(sizeof(double) * (size_t)k * ncls);
+  double* zz = (double*)malloc(sizeof(double) * (size_t)k * ncls);
+  double* da = (double*)malloc(sizeof(double) * (size_t)k * hidden);
+  double* lt = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+  int64_t correct = 0;
+  for (int r = 0; r < k; ++r) {
+    for (int j = 0; j < hidden; ++j) { /* h = tanh(x @ W1 + b1) */
+      double acc = 0.0;
+      for (int i = 0; i < n_in; ++i) acc = fma((double)x[r * n_in + i], (double)w[i * hidden + j], acc);
+      h[r * hidden + j] = tanh(acc + (double)w[o_b1 + j]);
+    }
+    double zmax = -INFINITY;
+    for (int c = 0; c < ncls; ++c) { /* z = h @ W2 + b2 */
+      double acc = 0.0;
+      for (int j = 0; j < hidden; ++j) acc = fma(h[r * hidden + j], (double)w[o_w2 + j * ncls + c], acc);
+      zz[r * ncls + c] = acc + (double)w[o_b2 + c];
+      if (zz[r * ncls + c] > zmax) zmax = zz[r * ncls + c];
+    }
+    double s = -0.0;
+    int arg = 0;
+    for (int c = 0; c < ncls; ++c) {
+      zz[r * ncls + c] = zz[r * ncls + c] - zmax;
+      if (zz[r * ncls + c] > zz[r * ncls + arg]) arg = c; /* argmax: first maximum */
+      pr[r * ncls + c] = exp(zz[r * ncls + c]);
+      s += pr[r * ncls + c];
+    }
+    for (int c = 0; c < ncls; ++c) pr[r * ncls + c] = pr[r * ncls + c] / s;
+    lt[r] = -log(pr[r * ncls + y[r]]);
+    correct += (arg == y[r]);
+    pr[r * ncls + y[r]] -= 1.0; /* dz */
+  }
+  double loss = 0.0 + np_pairwise(lt, k);
+  for (int r = 0; r < k; ++r) /* dh = dz @ W2.T; da = (1 - h*h) * dh */
+    for (int j = 0; j < hidden; ++j) {
+      double acc = 0.0;
+      for (int c = 0; c < ncls; ++c) acc = fma(pr[r * ncls + c], (double)w[o_w2 + j * ncls + c], acc);
+      double hv = h[r * hidden + j];
+      da[r * hidden + j] = (1.0 - hv * hv) * acc;
+    }
+  for (int i = 0; i < n_in; ++i) /* dW1 = x.T @ da */
+    for (int j = 0; j < hidden; ++j) {
+      double acc = 0.0;
+      for (int r = 0; r < k; ++r) acc = fma((double)x[r * n_in + i], da[r * hidden + j], acc);
+      out[i * hidden + j] = (float)acc;
+    }
+  for (int j = 0; j < hidden; ++j) { /* db1 = da.sum(0) */
+    double acc = 0.0;
+    for (int r = 0; r < k; ++r) acc += da[r * hidden + j];
+    out[o_b1 + j] = (float)acc;
+  }
+  for (int j = 0; j < hidden; ++j) /* dW2 = h.T @ dz */
+    for (int c = 0; c < ncls; ++c) {
+      double acc = 0.0;
+      for (int r = 0; r < k; ++r) acc = fma(h[r * hidden + j], pr[r * ncls + c], acc);
+      out[o_w2 + j * ncls + c] = (float)acc;
+    }
+  for (int c = 0; c < ncls; ++c) { /* db2 = dz.sum(0) */
+    double acc = 0.0;
+    for (int r = 0; r < k; ++r) acc += pr[r * ncls + c];
+    out[o_b2 + c] = (float)acc;
+  }
+  out[p] = (float)loss;
+  out[p + 1] = (float)correct;
+  free(h);
+  free(pr);
+  free(zz);
+  free(da);
+  free(lt);
 }

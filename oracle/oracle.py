@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
                                       C.c_int64, i64p, i32p, i64p]
         L.mo_shuffle_plan.restype = C.c_int64
         L.mo_random_batch.argtypes = [C.c_uint64, C.c_int64, C.c_int64, i64p]
+        L.mo_toy_grad.argtypes = [f32p, C.c_int, C.c_int, C.c_int, f32p, i64p, C.c_int, f32p]
         _lib = L
     return _lib
 
@@ -355,3 +356,19 @@ def allreduce_threads(tables, bufs: list[np.ndarray], weights=None, moms=None, u
 
 def fill_rank_input_c(buf: np.ndarray, rank: int, n_ranks: int) -> None:
     lib().mo_fill_rank_input(_f32p(buf), len(buf), rank, n_ranks)
+
+
+# -- the reference's gradient producer (sgd.py:148-248) -----------------------------------------
+
+
+def toy_grad_c(w: np.ndarray, n_in: int, hidden: int, n_classes: int, x: np.ndarray,
+               y: np.ndarray) -> np.ndarray:
+    """ToyModel.loss_and_grad_sum (sgd.py:220-248) as node_gradient's buffer
+    (sgd.py:335-353): [float32 gradient sum | loss sum | correct count]."""
+    w = np.ascontiguousarray(w, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.ascontiguousarray(y, np.int64)
+    out = np.zeros(w.size + 2, np.float32)
+    lib().mo_toy_grad(_f32p(w), n_in, hidden, n_classes, _f32p(x),
+                      y.ctypes.data_as(C.POINTER(C.c_int64)), int(y.size), _f32p(out))
+    return out

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libmdb200.so"
 SOURCES = ["md_elementwise.cu", "md_allreduce.cu", "md_ar_tree.cu", "md_ar_direct.cu", "md_ar_push.cu",
-           "md_dimd.cu"]
+           "md_dimd.cu", "md_toy.cu"]
 HEADERS = ["md_common.cuh", "md_allreduce.cuh", "../../include/mdb200.h"]
 
 NVCC_FLAGS = [

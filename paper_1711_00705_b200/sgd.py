@@ -11,9 +11,11 @@ multicolor allreduce and the weight update are ONE kernel launch
 (collectives.run_fold with ``workers`` + ``update``); the replica check is a
 device digest compared through the host channel.
 
-The model's forward/backward is outside the hot path (the reference uses a
-172-parameter toy MLP as a stand-in for ResNet-50, :147-247): ``train_step``
-takes a ``grad_fn`` producing per-worker gradient buffers. The momentum and
+The gradient producer is pluggable: ``train_step`` takes a ``grad_fn``
+writing per-worker gradient buffers; for the reference's own model
+(``model.ToyModel``, the 172-parameter MLP of :147-247) it defaults to the
+device producer ``md_toy_grad``, so ``run_training(cfg, corpus)`` runs the
+reference's whole training loop on the GPU with its bits. The momentum and
 weight-decay terms are an extension (the reference has plain SGD); with
 ``momentum == weight_decay == 0`` the update is bit-identical to
 ``sub_scaled_f32(W, g[:p], lr / B)``.
@@ -245,12 +247,16 @@ def train_step(
 
     ``grad_fn(model, batches, worker_bufs)`` writes each worker's summed
     gradient and its (loss sum, correct count) tail into ``worker_bufs[j]``
-    (p + 2 floats). With ``sync=False`` nothing waits on the device and the
+    (p + 2 floats); None = the device ToyModel producer (model.toy_grad_fn). With ``sync=False`` nothing waits on the device and the
     returned stats are None (the bench's device-resident loop)."""
     if ep.n_ranks != cfg.n_nodes:
         raise InvalidConfig(f"config says {cfg.n_nodes} nodes, running {ep.n_ranks}")
     if grad_fn is None:
-        raise InvalidConfig("train_step needs a grad_fn (the model is outside the hot path)")
+        from paper_1711_00705_b200.model import ToyModel, toy_grad_fn
+
+        if not isinstance(model, ToyModel):
+            raise InvalidConfig("train_step needs a grad_fn for a model other than ToyModel")
+        grad_fn = toy_grad_fn
     lr = lr_at(lr_schedule(cfg), epoch)
     p = model.n_params
     if buffers is None:
@@ -309,8 +315,8 @@ def run_training(
     corpus,
     algo: str = "multicolor",
     *,
-    grad_fn,
-    init_weights: np.ndarray,
+    grad_fn=None,
+    init_weights: np.ndarray | None = None,
     backend: str = "cuda",
     emulate: bool | None = None,
     record_bytes: int | None = None,
@@ -320,11 +326,12 @@ def run_training(
     Each epoch optionally reshuffles the DIMD store (``shuffle_all`` keyed
     ``_mix64(seed, "shuf", epoch)``), then runs max(1, len(corpus) //
     effective_batch) steps of ``train_step``; metrics are identical on every
-    rank and rank 0's copy is returned. The store, the shuffle, the fused
-    fold + allreduce + update and the replica check run on the GPU; the
-    model's forward/backward is ``grad_fn`` (the reference's ToyModel is a
-    stand-in outside the hot path), and ``init_weights`` replaces
-    ``ToyModel.create``.
+    rank and rank 0's copy is returned. The store, the shuffle, the gradient
+    producer, the fused fold + allreduce + update and the replica check run on
+    the GPU. By default the model is the reference's ``ToyModel`` (n_in = the
+    record size / 4, ``cfg.hidden`` units, 4 classes, ``ToyModel.create(seed=
+    cfg.seed)``) with the device producer; ``grad_fn`` + ``init_weights``
+    plug in another model.
     """
     from paper_1711_00705_b200.dimd import build_blob, parse_index, shard_from_bytes, shuffle_all
     from paper_1711_00705_b200.transport import run_ranks
@@ -334,7 +341,22 @@ def run_training(
     blob, index = build_blob(corpus)
     entries = parse_index(index)
     steps_per_epoch = max(1, len(corpus) // cfg.effective_batch)
-    w0 = np.ascontiguousarray(init_weights, dtype=np.float32)
+    toy = grad_fn is None
+    if toy:
+        from paper_1711_00705_b200.model import ToyModel
+
+        if init_weights is not None:
+            raise InvalidConfig("init_weights needs a grad_fn (the ToyModel initialises itself)")
+        n_in = len(corpus[0].bytes) // 4
+        record_bytes = len(corpus[0].bytes) if record_bytes is None else record_bytes
+        bad = [r.label for r in corpus if not -4 <= r.label < 4]
+        if bad:  # the reference fails on p[rows, y] (sgd.py:235)
+            raise IndexError(f"label {bad[0]} is out of range for the model's 4 classes")
+        w0 = ToyModel.init_weights(n_in, cfg.hidden, 4, cfg.seed)
+    elif init_weights is None:
+        raise InvalidConfig("a custom grad_fn needs init_weights")
+    else:
+        w0 = np.ascontiguousarray(init_weights, dtype=np.float32)
 
     def program(ep):
         import time
@@ -343,6 +365,9 @@ def run_training(
         with torch.cuda.device(dev), torch.cuda.stream(ep.stream):
             store = shard_from_bytes(blob, entries, ep.rank, ep.n_ranks, cfg.group_size, device=dev)
             model = DeviceModel.from_numpy(w0, dev, momentum=cfg.momentum != 0)
+            if toy:
+                model = ToyModel(model.weights, n_in=n_in, hidden=cfg.hidden, n_classes=4,
+                                 momentum=model.momentum)
             tree_set, ring = comm_plan(ep.n_ranks, algo)
             buffers = StepBuffers(ep, model.n_params, cfg.workers_per_node)
             t_start = time.perf_counter()
