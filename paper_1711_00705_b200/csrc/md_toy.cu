@@ -200,6 +200,9 @@ extern "C" int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t
   MD_CUDA_TRY(cudaGetDevice(&dev));
   int optin = 0;
   MD_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa{};
+  MD_CUDA_TRY(cudaFuncGetAttributes(&fa, md::toy_grad_kernel));
+  optin -= static_cast<int>(fa.sharedSizeBytes);  // the kernel's static shared memory
   if (smem > static_cast<size_t>(optin)) {
     md::set_error("md_toy_grad: batch %d x (%d in, %d hidden, %d classes) needs %zu B of shared "
                   "memory (> %d)", batch, n_in, hidden, n_classes, smem, optin);
