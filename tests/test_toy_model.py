@@ -17,6 +17,7 @@ import pytest
 from paper_1711_00705_b200 import TrainConfig, make_synthetic_corpus
 from paper_1711_00705_b200.model import ToyModel
 from paper_1711_00705_b200.sgd import SAMPLE_ROLE
+from tests.conftest import need_gpus
 
 ROOT = Path(__file__).resolve().parents[1]
 
@@ -175,22 +176,35 @@ def test_train_step_with_device_producer_matches_reference(golden, oracle):
             assert np.array_equal(w, golden["sgd_weights"][step]), (r, step)
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("t", [0, 1])
-def test_run_training_matches_reference(toy, t):
-    """run_training(cfg, corpus) (sgd.py:470-542) -- shuffles, device
-    ToyModel producer, fused allreduce + update, replica checks -- against
-    the reference's own run: final weights, every step's loss / correct / lr,
-    every epoch's metrics."""
+def _run_training_case(toy, t, emulate):
     from paper_1711_00705_b200 import run_training
 
     nn, m, kb, epochs, seed, nrec, hidden, every = (int(v) for v in toy[f"train{t}_cfg"])
     cfg = TrainConfig(n_nodes=nn, workers_per_node=m, per_worker_batch=kb, epochs=epochs,
                       seed=seed, hidden=hidden, shuffle_every=every)
     corpus = make_synthetic_corpus(nrec, seed=seed)
-    res = run_training(cfg, corpus, "multicolor", emulate=True)
+    res = run_training(cfg, corpus, "multicolor", emulate=emulate)
     assert np.array_equal(res.weights, toy[f"train{t}_weights"])
     got = np.array([[s.step, s.loss, s.correct, s.lr] for s in res.steps])
     assert np.array_equal(got, toy[f"train{t}_steps"])
     hist = np.array([[h.epoch, h.loss, h.acc] for h in res.history])
     assert np.array_equal(hist, toy[f"train{t}_history"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("t", [0, 1])
+def test_run_training_matches_reference(toy, t):
+    """run_training(cfg, corpus) (sgd.py:470-542) -- shuffles, device
+    ToyModel producer, fused allreduce + update, replica checks -- against
+    the reference's own run: final weights, every step's loss / correct / lr,
+    every epoch's metrics. Ranks emulated on one GPU."""
+    _run_training_case(toy, t, emulate=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+@need_gpus(4)
+@pytest.mark.parametrize("t", [0, 1])
+def test_run_training_matches_reference_one_gpu_per_rank(toy, t):
+    """The same runs with one GPU per rank (NVLink peers)."""
+    _run_training_case(toy, t, emulate=False)
