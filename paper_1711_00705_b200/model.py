@@ -94,10 +94,13 @@ class ToyModel:
             if r.dtype != torch.uint8 or r.dim() != 2 or r.shape[0] != k or r.stride(0) != stride \
                     or r.stride(1) != 1 or r.device != self.weights.device:
                 raise InvalidConfig("worker records must be uint8 [k, L] rows on the model's device")
-            if lab.dtype != torch.int32 or lab.numel() != k or not lab.is_contiguous():
-                raise InvalidConfig("worker labels must be k contiguous int32")
-            if o.dtype != torch.float32 or o.numel() != self.n_params + 2 or not o.is_contiguous():
-                raise InvalidConfig(f"gradient buffers must be {self.n_params + 2} contiguous float32")
+            if lab.dtype != torch.int32 or lab.numel() != k or not lab.is_contiguous() \
+                    or lab.device != self.weights.device:
+                raise InvalidConfig("worker labels must be k contiguous int32 on the model's device")
+            if o.dtype != torch.float32 or o.numel() != self.n_params + 2 or not o.is_contiguous() \
+                    or o.device != self.weights.device:
+                raise InvalidConfig(f"gradient buffers must be {self.n_params + 2} contiguous "
+                                    "float32 on the model's device")
         if int(recs[0].shape[1]) < feature_bytes * self.n_in:
             raise InvalidConfig(f"expected {self.n_in} features, records hold "
                                 f"{int(recs[0].shape[1]) // feature_bytes}")
