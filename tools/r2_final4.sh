@@ -1,0 +1,13 @@
+# round-2 final pass after the ToyModel producer landed (one 4-GPU box):
+# all GPU tests incl. multi-GPU, smoke, C5 bench N=1/2/4 + reference arm
+R="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+O=gpurun_out/final4; mkdir -p $O
+nvidia-smi -L > $O/smi.txt
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $O/pytest.txt
+timeout 900 python -m pytest tests -m multigpu -v 2>&1 | grep -E "PASSED|FAILED|SKIPPED|ERROR|passed|failed" > $O/pytest_multigpu_list.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
+timeout 400 python bench.py > $O/b1.json 2> $O/b1.err
+timeout 400 $R --nproc-per-node 2 --master-port 29601 bench.py --gpus 2 > $O/b2.json 2> $O/b2.err
+timeout 400 $R --nproc-per-node 4 --master-port 29602 bench.py --gpus 4 > $O/b4.json 2> $O/b4.err
+timeout 400 python bench.py --impl reference > $O/r1.json 2> $O/r1.err
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi_end.txt
