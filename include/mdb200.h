@@ -342,7 +342,7 @@ int md_digest_f32(const float* x, int64_t n, uint64_t* digest, void* stream);
  * labels[j]: int32 class
  * indices (negative ones wrap like numpy indices); records / labels / out are
  * HOST arrays of n_workers DEVICE pointers. status (device, nullable) gets
- * 1 + the first row whose label is out of range (the reference's IndexError).
+ * 1 + the index of a row whose label is out of range (the reference's IndexError).
  * MD_ERR_LENGTH_MISMATCH if record_stride < feature_bytes*n_in; MD_ERR_INVALID_CONFIG if
  * the batch does not fit one CTA's shared memory. */
 int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t n_classes,

@@ -34,7 +34,7 @@ struct ToyArgs {
   const uint8_t* records[MD_MAX_WORKERS];
   const int32_t* labels[MD_MAX_WORKERS];
   float* out[MD_MAX_WORKERS];
-  int32_t* status;  // nullable: 1 + first row whose label is out of range
+  int32_t* status;  // nullable: 1 + a row whose label is out of range (the first to report)
 };
 
 // numpy's pairwise_sum (umath/loops_utils.h.src) over n float64 values
