@@ -572,13 +572,18 @@ struct PushArgs {
 
 // Work item i -> receiver (me + 1 + i mod S) mod S, entry i / S of our list
 // there: every CTA wave spreads its stores over all receivers (a wave that
-// targets one receiver would queue on that GPU's ingress).
+// targets one receiver would queue on that GPU's ingress). Thread 0 runs the
+// items' metadata two steps ahead (the list entry of item i + 2G, the source
+// offset of item i + G -- two dependent loads), so the chain's latency is off
+// the copy's path, as in gather_kernel.
 __global__ void __launch_bounds__(512) push_kernel(const __grid_constant__ PushArgs p, int32_t S,
                                                    int32_t me, const uint8_t* blob,
                                                    const uint64_t* off) {
   __shared__ int64_t lo[MD_MAX_GROUP], cnt[MD_MAX_GROUP];
   __shared__ int64_t s_items;
   __shared__ SendEntry s_e;
+  __shared__ uint64_t s_src;
+  __shared__ int s_ok;
   const int tid = threadIdx.x;
   if (tid < S) {
     const int64_t* b = p.begin[tid];
@@ -593,15 +598,41 @@ __global__ void __launch_bounds__(512) push_kernel(const __grid_constant__ PushA
   }
   __syncthreads();
   const int64_t items = s_items;
-  for (int64_t i = blockIdx.x; i < items; i += gridDim.x) {
+  const int64_t G = gridDim.x;
+  auto fetch = [&](int64_t i, SendEntry* en) -> bool {
+    if (i >= items) return false;
     const int d = (me + 1 + static_cast<int>(i % S)) % S;
     const int64_t e = i / S;
-    if (e >= cnt[d]) continue;  // uniform across the CTA
-    if (tid == 0) s_e = p.list[d][lo[d] + e];
+    if (e >= cnt[d]) return false;
+    *en = p.list[d][lo[d] + e];
+    return true;
+  };
+  SendEntry e_cur{}, e_next{};
+  uint64_t o_cur = 0;
+  bool v_cur = false, v_next = false;
+  if (tid == 0) {
+    v_cur = fetch(blockIdx.x, &e_cur);
+    o_cur = v_cur ? off[e_cur.src_rec] : 0;
+    v_next = fetch(blockIdx.x + G, &e_next);
+  }
+  for (int64_t i = blockIdx.x; i < items; i += G) {
+    if (tid == 0) {
+      s_e = e_cur;
+      s_src = o_cur;
+      s_ok = v_cur;
+      // advance the pipeline: offset of the next item, entry of the one after
+      o_cur = v_next ? off[e_next.src_rec] : 0;
+      e_cur = e_next;
+      v_cur = v_next;
+      v_next = fetch(i + 2 * G, &e_next);
+    }
     __syncthreads();
-    const SendEntry en = s_e;
-    cta_copy(p.out[d] + en.dst_off, blob + off[en.src_rec], en.len);
-    __syncthreads();  // s_e is rewritten by the next item
+    if (s_ok) {  // uniform across the CTA
+      const int d = (me + 1 + static_cast<int>(i % S)) % S;
+      const SendEntry en = s_e;
+      cta_copy(p.out[d] + en.dst_off, blob + s_src, en.len);
+    }
+    __syncthreads();  // s_e / s_src are rewritten by the next item
   }
 }
 
