@@ -576,7 +576,13 @@ struct PushArgs {
 // items' metadata two steps ahead (the list entry of item i + 2G, the source
 // offset of item i + G -- two dependent loads), so the chain's latency is off
 // the copy's path, as in gather_kernel.
-__global__ void __launch_bounds__(512) push_kernel(const __grid_constant__ PushArgs p, int32_t S,
+// kLocal: the one-member instance (S == 1, copies within the own HBM) is
+// capped at 32 registers for 4 resident CTAs per SM (A/B: epoch 8.72 -> 8.39
+// ms at N = 1); across GPUs the 64-register instance (2 CTAs per SM, the
+// exchange grid) is faster (19.0 vs 19.3 ms at N = 2): the links, not the
+// SM's loads in flight, bound it there.
+template <bool kLocal>
+__global__ void __launch_bounds__(512, kLocal ? 4 : 2) push_kernel(const __grid_constant__ PushArgs p, int32_t S,
                                                    int32_t me, const uint8_t* blob,
                                                    const uint64_t* off) {
   __shared__ int64_t lo[MD_MAX_GROUP], cnt[MD_MAX_GROUP];
@@ -1268,8 +1274,11 @@ int md_shuffle_push(int32_t S, int32_t member, const uint8_t* blob, const uint64
   // (work items are records, many per CTA: the full exchange grid; a
   // one-member group only copies within its own HBM, where the record-copy
   // grid's second wave of CTAs evens out the tail)
-  const int grid = S == 1 ? record_grid(INT64_MAX) : exchange_grid(INT64_MAX);
-  push_kernel<<<grid, 512, 0, as_stream(stream)>>>(p, S, member, blob, off);
+  if (S == 1)
+    push_kernel<true><<<record_grid(INT64_MAX), 512, 0, as_stream(stream)>>>(p, S, member, blob, off);
+  else
+    push_kernel<false><<<exchange_grid(INT64_MAX), 512, 0, as_stream(stream)>>>(p, S, member, blob,
+                                                                               off);
   MD_LAUNCH_CHECK();
   return MD_OK;
 }
