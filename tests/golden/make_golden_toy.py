@@ -10,8 +10,8 @@ Records
     record values), labels, the float32 gradient, the loss sum, the count;
   * ``grad_*``: grad(model, batch) (sgd.py:250-257) on float64 features;
   * ``train_*``: run_training (sim backend) of make_synthetic_corpus records
-    for two configurations, with reshuffles -- final weights and every step's
-    (loss, correct, lr).
+    for four configurations (multicolor / ring / reduce_bcast, shuffle groups),
+    with reshuffles -- final weights and every step's (loss, correct, lr).
 Everything recorded is an output of reference code (make_golden.py's import
 recipe: scratch copy, thread-backed greenlet stand-in).
 """
@@ -33,9 +33,12 @@ SHAPES = [  # (batch, n_in, hidden, classes, seed)
     (3, 40, 32, 7, 14), (64, 8, 2, 3, 15),
 ]
 
-TRAIN = [  # (n_nodes, workers, per_worker_batch, epochs, seed, n_records, hidden, shuffle_every)
-    (2, 2, 4, 3, 5, 96, 8, 1),
-    (4, 1, 8, 2, 11, 160, 6, 2),
+TRAIN = [  # (n_nodes, workers, per_worker_batch, epochs, seed, n_records, hidden, shuffle_every,
+    #    group_size, algo)
+    (2, 2, 4, 3, 5, 96, 8, 1, 1, "multicolor"),
+    (4, 1, 8, 2, 11, 160, 6, 2, 1, "multicolor"),
+    (3, 2, 3, 2, 17, 120, 5, 1, 3, "ring"),
+    (4, 1, 4, 2, 23, 100, 8, 1, 2, "reduce_bcast"),
 ]
 
 
@@ -71,12 +74,13 @@ def main() -> None:
     G["grad_y"] = labels.astype(np.int64)
     G["grad_out"] = np.asarray(grad(model, list(zip(feats, labels.tolist()))).data, np.float32)
 
-    for j, (nn, m, kb, epochs, seed, nrec, hidden, every) in enumerate(TRAIN):
+    for j, (nn, m, kb, epochs, seed, nrec, hidden, every, gs, algo) in enumerate(TRAIN):
         cfg = TrainConfig(n_nodes=nn, workers_per_node=m, per_worker_batch=kb, epochs=epochs,
-                          seed=seed, hidden=hidden, shuffle_every=every)
+                          seed=seed, hidden=hidden, shuffle_every=every, group_size=gs)
         corpus = make_synthetic_corpus(nrec, seed=seed)
-        res = run_training(cfg, corpus, "multicolor", backend="sim")
-        G[f"train{j}_cfg"] = np.array([nn, m, kb, epochs, seed, nrec, hidden, every], np.int64)
+        res = run_training(cfg, corpus, algo, backend="sim")
+        G[f"train{j}_cfg"] = np.array([nn, m, kb, epochs, seed, nrec, hidden, every, gs], np.int64)
+        G[f"train{j}_algo"] = np.array(algo)
         G[f"train{j}_corpus_x"] = np.stack([np.frombuffer(r.bytes, "<f4") for r in corpus])
         G[f"train{j}_corpus_y"] = np.array([r.label for r in corpus], np.int64)
         G[f"train{j}_weights"] = np.asarray(res.weights, np.float32)

@@ -74,7 +74,7 @@ def test_oracle_reproduces_golden_worker_buffers(golden, oracle):
 
 def test_host_helpers_match_reference(toy):
     for t in range(int(toy["n_train"][0])):
-        _, _, _, _, seed, nrec, _, _ = (int(v) for v in toy[f"train{t}_cfg"])
+        seed, nrec = int(toy[f"train{t}_cfg"][4]), int(toy[f"train{t}_cfg"][5])
         corpus = make_synthetic_corpus(nrec, seed=seed)
         xs = np.stack([np.frombuffer(r.bytes, "<f4") for r in corpus])
         assert np.array_equal(xs.view(np.uint32), toy[f"train{t}_corpus_x"].view(np.uint32))
@@ -179,11 +179,11 @@ def test_train_step_with_device_producer_matches_reference(golden, oracle):
 def _run_training_case(toy, t, emulate):
     from paper_1711_00705_b200 import run_training
 
-    nn, m, kb, epochs, seed, nrec, hidden, every = (int(v) for v in toy[f"train{t}_cfg"])
+    nn, m, kb, epochs, seed, nrec, hidden, every, gs = (int(v) for v in toy[f"train{t}_cfg"])
     cfg = TrainConfig(n_nodes=nn, workers_per_node=m, per_worker_batch=kb, epochs=epochs,
-                      seed=seed, hidden=hidden, shuffle_every=every)
+                      seed=seed, hidden=hidden, shuffle_every=every, group_size=gs)
     corpus = make_synthetic_corpus(nrec, seed=seed)
-    res = run_training(cfg, corpus, "multicolor", emulate=emulate)
+    res = run_training(cfg, corpus, str(toy[f"train{t}_algo"]), emulate=emulate)
     assert np.array_equal(res.weights, toy[f"train{t}_weights"])
     got = np.array([[s.step, s.loss, s.correct, s.lr] for s in res.steps])
     assert np.array_equal(got, toy[f"train{t}_steps"])
@@ -191,8 +191,12 @@ def _run_training_case(toy, t, emulate):
     assert np.array_equal(hist, toy[f"train{t}_history"])
 
 
+TRAIN_CASES = [0, 1, 2, 3]  # multicolor x2, ring (3 nodes, one shuffle group of 3),
+#                             reduce_bcast (4 nodes, shuffle groups of 2)
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("t", [0, 1])
+@pytest.mark.parametrize("t", TRAIN_CASES)
 def test_run_training_matches_reference(toy, t):
     """run_training(cfg, corpus) (sgd.py:470-542) -- shuffles, device
     ToyModel producer, fused allreduce + update, replica checks -- against
@@ -204,7 +208,7 @@ def test_run_training_matches_reference(toy, t):
 @pytest.mark.gpu
 @pytest.mark.multigpu
 @need_gpus(4)
-@pytest.mark.parametrize("t", [0, 1])
+@pytest.mark.parametrize("t", TRAIN_CASES)
 def test_run_training_matches_reference_one_gpu_per_rank(toy, t):
     """The same runs with one GPU per rank (NVLink peers)."""
     _run_training_case(toy, t, emulate=False)
