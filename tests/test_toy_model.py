@@ -212,3 +212,23 @@ def test_run_training_matches_reference(toy, t):
 def test_run_training_matches_reference_one_gpu_per_rank(toy, t):
     """The same runs with one GPU per rank (NVLink peers)."""
     _run_training_case(toy, t, emulate=False)
+
+
+@pytest.mark.gpu
+def test_device_toy_grad_many_workers_one_call(oracle):
+    """grad_into with more workers than one launch holds (MD_MAX_WORKERS = 8):
+    every worker's buffer equals the oracle's."""
+    import torch
+
+    rng = np.random.default_rng(44)
+    model = ToyModel.create(n_in=12, hidden=6, n_classes=5, seed=8)
+    w = model.weights.cpu().numpy()
+    xs = [rng.standard_normal((7, 12)).astype("<f4") for _ in range(11)]
+    ys = [rng.integers(0, 5, size=7) for _ in range(11)]
+    batches = [(torch.from_numpy(x.view(np.uint8).copy()).cuda(),
+                torch.from_numpy(y.astype(np.int32)).cuda()) for x, y in zip(xs, ys)]
+    outs = [torch.empty(model.n_params + 2, dtype=torch.float32, device="cuda") for _ in xs]
+    model.grad_into(batches, outs)
+    for x, y, o in zip(xs, ys, outs):
+        want = oracle.toy_grad_c(w, 12, 6, 5, x, y)
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), want.view(np.uint32))
