@@ -13,7 +13,7 @@ the host, once.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -40,6 +40,7 @@ class ToyModel:
     hidden: int = 8
     n_classes: int = 4
     momentum: torch.Tensor | None = None
+    _work: torch.Tensor | None = field(default=None, repr=False, compare=False)
 
     def __post_init__(self):
         w = self.weights
@@ -104,10 +105,17 @@ class ToyModel:
         if int(recs[0].shape[1]) < feature_bytes * self.n_in:
             raise InvalidConfig(f"expected {self.n_in} features, records hold "
                                 f"{int(recs[0].shape[1]) // feature_bytes}")
+        lib = _lib.load()
+        nbytes = int(lib.md_toy_work_bytes(self.hidden, self.n_classes, k))
+        if self._work is None or self._work.numel() * 8 < nbytes \
+                or self._work.device != self.weights.device:
+            self._work = torch.empty((nbytes + 7) // 8, dtype=torch.float64,
+                                     device=self.weights.device)
         _lib.check(
-            _lib.load().md_toy_grad(
+            lib.md_toy_grad(
                 self.weights.data_ptr(), self.n_in, self.hidden, self.n_classes,
                 _ptrs(recs), feature_bytes, _ptrs(labs), stride, k, _ptrs(outs), len(outs),
+                self._work.data_ptr(), self._work.numel() * 8,
                 None if status is None else status.data_ptr(),
                 _lib.stream_ptr(torch.cuda.current_stream(self.weights.device)),
             )

@@ -31,6 +31,7 @@ SHAPES = [  # (batch, n_in, hidden, classes, seed)
     (9, 16, 8, 4, 6), (32, 16, 8, 4, 7), (128, 16, 8, 4, 8), (129, 16, 8, 4, 9),
     (300, 16, 8, 4, 10), (5, 3, 5, 2, 11), (6, 1, 1, 1, 12), (16, 24, 12, 10, 13),
     (3, 40, 32, 7, 14), (64, 8, 2, 3, 15),
+    (8, 16, 2048, 4, 16),  # the reference's bench_train model (bench.py:71-75)
 ]
 
 TRAIN = [  # (n_nodes, workers, per_worker_batch, epochs, seed, n_records, hidden, shuffle_every,
@@ -39,6 +40,7 @@ TRAIN = [  # (n_nodes, workers, per_worker_batch, epochs, seed, n_records, hidde
     (4, 1, 8, 2, 11, 160, 6, 2, 1, "multicolor"),
     (3, 2, 3, 2, 17, 120, 5, 1, 3, "ring"),
     (4, 1, 4, 2, 23, 100, 8, 1, 2, "reduce_bcast"),
+    (4, 2, 8, 2, 29, 512, 2048, 1, 1, "multicolor"),  # bench_train's model width
 ]
 
 

@@ -80,7 +80,7 @@ def test_host_helpers_match_reference(toy):
         assert np.array_equal(xs.view(np.uint32), toy[f"train{t}_corpus_x"].view(np.uint32))
         assert [r.label for r in corpus] == toy[f"train{t}_corpus_y"].tolist()
     for i, k, n_in, h, c in _cases(toy):
-        seed = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15][i]
+        seed = i + 1  # make_golden_toy.py SHAPES
         assert np.array_equal(ToyModel.init_weights(n_in, h, c, seed), toy[f"case{i}_w"]), i
 
 
@@ -191,8 +191,8 @@ def _run_training_case(toy, t, emulate):
     assert np.array_equal(hist, toy[f"train{t}_history"])
 
 
-TRAIN_CASES = [0, 1, 2, 3]  # multicolor x2, ring (3 nodes, one shuffle group of 3),
-#                             reduce_bcast (4 nodes, shuffle groups of 2)
+TRAIN_CASES = [0, 1, 2, 3, 4]  # multicolor x2, ring (3 nodes, one shuffle group of 3),
+#   reduce_bcast (4 nodes, shuffle groups of 2), bench_train's 16 -> 2048 -> 4 model
 
 
 @pytest.mark.gpu
