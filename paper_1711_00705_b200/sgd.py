@@ -150,15 +150,18 @@ class StepStats:
 
 
 def sample_node_batch(store: ShardStore, cfg: TrainConfig, rank: int, step: int,
-                      record_bytes: int | None = None):
+                      record_bytes: int | None = None, slots=None):
     """Per-worker sub-batches carved at the source (sgd.py:290-314): worker j
     of rank r is global worker r*m+j, keyed _mix64(seed, "samp", worker, step).
-    Returns [(records uint8 [k, L], labels int32 [k], picks int64 [k])]."""
+    Returns [(records uint8 [k, L], labels int32 [k], picks int64 [k])].
+    With ``slots`` (one dimd.BatchSlots per worker) nothing is allocated and
+    nothing waits; the caller checks ``slots[j].err``."""
     out = []
     for j in range(cfg.workers_per_node):
         worker = rank * cfg.workers_per_node + j
         key = _mix64(cfg.seed, SAMPLE_ROLE, worker, step)
-        out.append(random_batch_device(store, BatchRequest(cfg.per_worker_batch, key), record_bytes))
+        out.append(random_batch_device(store, BatchRequest(cfg.per_worker_batch, key),
+                                       record_bytes, None if slots is None else slots[j]))
     return out
 
 
@@ -223,6 +226,18 @@ class StepBuffers:
         dev = ep.torch_device
         self.workers = [torch.zeros(n_params + 2, dtype=torch.float32, device=dev)
                         for _ in range(workers)]
+        self._slots: dict = {}
+        # per-step readback: (loss sum, correct count) + every worker's batch error word
+        self.host = torch.zeros(2 + workers, dtype=torch.float32).pin_memory()
+
+    def slots(self, batch: int, record_bytes: int, device):
+        """One preallocated minibatch slot set per worker (no per-step allocation)."""
+        from paper_1711_00705_b200.dimd import BatchSlots
+
+        key = (batch, record_bytes)
+        if key not in self._slots:
+            self._slots[key] = [BatchSlots(batch, record_bytes, device) for _ in self.workers]
+        return self._slots[key]
 
 
 def train_step(
@@ -261,7 +276,9 @@ def train_step(
     p = model.n_params
     if buffers is None:
         buffers = StepBuffers(ep, p, cfg.workers_per_node)
-    batches = sample_node_batch(store, cfg, ep.rank, step, record_bytes)
+    slots = (buffers.slots(cfg.per_worker_batch, record_bytes, store.device)
+             if record_bytes is not None else None)
+    batches = sample_node_batch(store, cfg, ep.rank, step, record_bytes, slots)
     grad_fn(model, batches, buffers.workers)
     b = cfg.effective_batch
     upd = SgdUpdate(
@@ -274,15 +291,26 @@ def train_step(
     )
     allreduce(
         ep, buffers.grad, algo, tree_set=tree_set, ring=ring, segment_elems=segment_elems,
-        workers=buffers.workers, update=upd, check=sync,
+        workers=buffers.workers, update=upd, check=False,
     )
     if not sync:
         return model, None
+    # one wait per step: the metric slots and the batches' error words come
+    # back together, then the collective's error word (host-mapped)
+    host = buffers.host
+    host[0:2].copy_(buffers.grad.data[p : p + 2], non_blocking=True)
+    if slots is not None:
+        for j, sl in enumerate(slots):
+            host[2 + j : 3 + j].copy_(sl.err, non_blocking=True)  # int32 -> float32 value
+    torch.cuda.current_stream(ep.torch_device).synchronize()
+    ep.take_error()
+    if slots is not None and bool((host[2:] != 0).any()):
+        for sl in slots:
+            sl.check()  # raises LengthMismatch
     if verify_replicas:
         check_replicas(ep, model.weights, step)
-    tail = buffers.grad.data[p : p + 2].cpu().numpy()
-    stats = StepStats(step=step, epoch=epoch, lr=lr, loss=float(tail[0]) / b,
-                      correct=int(tail[1]), samples=b)
+    stats = StepStats(step=step, epoch=epoch, lr=lr, loss=float(host[0]) / b,
+                      correct=int(host[1]), samples=b)
     return model, stats
 
 
