@@ -341,13 +341,14 @@ int md_digest_f32(const float* x, int64_t n, uint64_t* digest, void* stream);
  * 4: the DIMD records, sgd.py:310-313) or float64 (8: grad(), sgd.py:250-257);
  * labels[j]: int32 class indices (negative ones wrap like numpy indices);
  * records / labels / out are HOST arrays of n_workers DEVICE pointers.
- * work: device workspace of at least md_toy_work_bytes(hidden, n_classes,
- * batch) bytes, 8-byte aligned (the float64 intermediates; any model size).
+ * work: device workspace of at least md_toy_work_bytes(n_in, hidden,
+ * n_classes, batch) bytes, 8-byte aligned (the float64 intermediates; any
+ * model size).
  * status (device, nullable) gets 1 + the index of a row whose label is out of
  * range (the reference's IndexError).
  * MD_ERR_LENGTH_MISMATCH if record_stride < feature_bytes*n_in;
  * MD_ERR_INVALID_CONFIG for a short workspace. */
-int64_t md_toy_work_bytes(int32_t hidden, int32_t n_classes, int32_t batch);
+int64_t md_toy_work_bytes(int32_t n_in, int32_t hidden, int32_t n_classes, int32_t batch);
 int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t n_classes,
                 const uint8_t* const* records, int32_t feature_bytes,
                 const int32_t* const* labels, int64_t record_stride, int32_t batch,

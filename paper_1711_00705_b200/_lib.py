@@ -107,7 +107,7 @@ SIGNATURES = {
         C.c_int, [_vp, _vp, _vp, _vp, _i64, _u64, C.c_uint32, _vp, C.POINTER(_i64), _vp]
     ),
     "md_digest_f32": (C.c_int, [_vp, _i64, C.POINTER(_u64), _vp]),
-    "md_toy_work_bytes": (_i64, [_i32, _i32, _i32]),
+    "md_toy_work_bytes": (_i64, [_i32, _i32, _i32, _i32]),
     "md_toy_grad": (C.c_int, [_vp, _i32, _i32, _i32, _pp, _i32, _pp, _i64, _i32, _pp, _i32, _vp,
                               _i64, _vp, _vp]),
 }

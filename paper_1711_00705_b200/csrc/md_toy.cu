@@ -14,8 +14,9 @@
 //   * softmax row sums sequential, column sums (axis 0) sequential over rows,
 //     the loss sum numpy's pairwise summation;
 //   * argmax = first maximum; labels wrap like numpy indices (y < 0 -> y + C).
-// Five small launches per step, each parallel over (worker, output element):
-// hidden layer, logits, softmax rows, hidden gradient, parameter gradients.
+// Six small launches per step, parallel over (worker, output element): input
+// conversion, hidden layer, logits (one CTA per row, operands staged in shared
+// memory), softmax rows, hidden gradient, parameter gradients.
 // Intermediates live in a caller-provided float64 workspace, so any model
 // size works (the reference's bench_train default is 16 -> 2048 -> 4).
 #include <cuda_runtime.h>
@@ -34,7 +35,7 @@ struct ToyArgs {
   int32_t feature_bytes;  // 4: float32 records (the DIMD format), 8: float64 features
   int64_t record_stride;
   int64_t work_stride;    // doubles of workspace per worker
-  double* work;           // [worker][h | z/p/dz | da | lt | lab | correct]
+  double* work;           // [worker][x | h | z/p/dz | da | lt | lab | correct]
   const uint8_t* records[MD_MAX_WORKERS];
   const int32_t* labels[MD_MAX_WORKERS];
   float* out[MD_MAX_WORKERS];
@@ -42,7 +43,7 @@ struct ToyArgs {
 };
 
 struct Work {
-  double *h, *pr, *da, *lt;
+  double *x, *h, *pr, *da, *lt;
   int* lab;
   int* correct;
 };
@@ -51,7 +52,8 @@ __device__ __forceinline__ Work work_of(const ToyArgs& a, int wk) {
   const int64_t k = a.batch, H = a.hidden, C = a.ncls;
   double* b = a.work + wk * a.work_stride;
   Work w;
-  w.h = b;                 // [k][H]
+  w.x = b;                 // [k][n_in]: the features as float64
+  w.h = w.x + k * a.n_in;  // [k][H]
   w.pr = w.h + k * H;      // [k][C]: z, then p, then dz
   w.da = w.pr + k * C;     // [k][H]
   w.lt = w.da + k * H;     // [k]: -log p[y]
@@ -60,8 +62,8 @@ __device__ __forceinline__ Work work_of(const ToyArgs& a, int wk) {
   return w;
 }
 
-int64_t work_doubles(int64_t k, int64_t H, int64_t C) {
-  return k * (2 * H + C + 1) + (k + 2 + 1) / 2;
+int64_t work_doubles(int64_t k, int64_t n_in, int64_t H, int64_t C) {
+  return k * (n_in + 2 * H + C + 1) + (k + 2 + 1) / 2;
 }
 
 // feature i of row r, as float64 (little endian; the records are byte rows)
@@ -111,19 +113,14 @@ __device__ double np_pairwise(const double* v, int64_t n) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; \
        e < (count); e += static_cast<int64_t>(gridDim.x) * blockDim.x)
 
-// 1. labels; h = tanh(x @ W1 + b1)
-__global__ void __launch_bounds__(kToyThreads) toy_hidden_kernel(const __grid_constant__ ToyArgs a) {
+// 1. features as float64, labels
+__global__ void __launch_bounds__(kToyThreads) toy_input_kernel(const __grid_constant__ ToyArgs a) {
   const int wk = blockIdx.y;
   const Work w = work_of(a, wk);
-  const int k = a.batch, n_in = a.n_in, H = a.hidden, C = a.ncls;
+  const int k = a.batch, n_in = a.n_in, C = a.ncls;
   const uint8_t* rec = a.records[wk];
-  TOY_LOOP(e, static_cast<int64_t>(k) * H) {
-    const int64_t r = e / H;
-    const int j = static_cast<int>(e % H);
-    double acc = 0.0;
-    for (int i = 0; i < n_in; ++i)
-      acc = fma(feat(a, rec, r, i), wv(a, static_cast<int64_t>(i) * H + j), acc);
-    w.h[e] = tanh(__dadd_rn(acc, wv(a, static_cast<int64_t>(n_in) * H + j)));
+  TOY_LOOP(e, static_cast<int64_t>(k) * n_in) {
+    w.x[e] = feat(a, rec, e / n_in, static_cast<int>(e % n_in));
   }
   TOY_LOOP(r, k) {
     int y = a.labels[wk][r];
@@ -137,23 +134,77 @@ __global__ void __launch_bounds__(kToyThreads) toy_hidden_kernel(const __grid_co
   }
 }
 
-// 2. z = h @ W2 + b2
-__global__ void __launch_bounds__(kToyThreads) toy_logits_kernel(const __grid_constant__ ToyArgs a) {
+// 2. h = tanh(x @ W1 + b1); the loads of a chain do not depend on it, so the
+// unrolled loop keeps them in flight ahead of the fused multiply-adds
+__global__ void __launch_bounds__(kToyThreads) toy_hidden_kernel(const __grid_constant__ ToyArgs a) {
   const Work w = work_of(a, blockIdx.y);
-  const int k = a.batch, n_in = a.n_in, H = a.hidden, C = a.ncls;
-  const int64_t o_w2 = static_cast<int64_t>(n_in) * H + H;
-  const int64_t o_b2 = o_w2 + static_cast<int64_t>(H) * C;
-  TOY_LOOP(e, static_cast<int64_t>(k) * C) {
-    const int64_t r = e / C;
-    const int c = static_cast<int>(e % C);
+  const int k = a.batch, n_in = a.n_in, H = a.hidden;
+  TOY_LOOP(e, static_cast<int64_t>(k) * H) {
+    const int64_t r = e / H;
+    const int j = static_cast<int>(e % H);
+    const double* xr = w.x + r * n_in;
     double acc = 0.0;
-    for (int j = 0; j < H; ++j)
-      acc = fma(w.h[r * H + j], wv(a, o_w2 + static_cast<int64_t>(j) * C + c), acc);
-    w.pr[e] = __dadd_rn(acc, wv(a, o_b2 + c));
+#pragma unroll 8
+    for (int i = 0; i < n_in; ++i) acc = fma(xr[i], wv(a, static_cast<int64_t>(i) * H + j), acc);
+    w.h[e] = tanh(__dadd_rn(acc, wv(a, static_cast<int64_t>(n_in) * H + j)));
   }
 }
 
-// 3. per row: softmax, -log p[y], argmax, dz = p - onehot(y)
+// 3. z = h @ W2 + b2: one CTA per (row, worker); the row of h and the W2 rows
+// are staged through shared memory in chunks, so each class's long
+// sequential chain (H fused multiply-adds) reads on-chip operands
+__global__ void __launch_bounds__(kToyThreads) toy_logits_kernel(const __grid_constant__ ToyArgs a,
+                                                                 int jc) {
+  extern __shared__ __align__(16) double st[];
+  const Work w = work_of(a, blockIdx.y);
+  const int n_in = a.n_in, H = a.hidden, C = a.ncls;
+  const int64_t r = blockIdx.x;
+  const int64_t o_w2 = static_cast<int64_t>(n_in) * H + H;
+  const int64_t o_b2 = o_w2 + static_cast<int64_t>(H) * C;
+  double* hs = st;                                   // [jc]
+  float* ws = reinterpret_cast<float*>(st + jc);     // [jc][C]
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // each thread owns classes c = tid, tid + nt, ... (C is small: one pass)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c0 = 0; c0 < C; c0 += 4 * nt) {
+    for (int j0 = 0; j0 < H; j0 += jc) {
+      const int n = min(jc, H - j0);
+      __syncthreads();
+      for (int t = tid; t < n; t += nt) hs[t] = w.h[r * H + j0 + t];
+      for (int t = tid; t < n * C; t += nt) ws[t] = __ldg(a.w + o_w2 + static_cast<int64_t>(j0) * C + t);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + tid + q * nt;
+        if (c < C) {
+          double v = acc[q];
+          // 16 operand pairs loaded ahead of their 16 chained multiply-adds
+          int t = 0;
+          for (; t + 16 <= n; t += 16) {
+            double hv[16], wq[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              hv[u] = hs[t + u];
+              wq[u] = static_cast<double>(ws[(t + u) * C + c]);
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) v = fma(hv[u], wq[u], v);
+          }
+          for (; t < n; ++t) v = fma(hs[t], static_cast<double>(ws[t * C + c]), v);
+          acc[q] = v;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + tid + q * nt;
+      if (c < C) w.pr[r * C + c] = __dadd_rn(acc[q], wv(a, o_b2 + c));
+      acc[q] = 0.0;
+    }
+  }
+}
+
+// 4. per row: softmax, -log p[y], argmax, dz = p - onehot(y)
 __global__ void __launch_bounds__(kToyThreads) toy_softmax_kernel(const __grid_constant__ ToyArgs a) {
   const Work w = work_of(a, blockIdx.y);
   const int k = a.batch, C = a.ncls;
@@ -179,7 +230,7 @@ __global__ void __launch_bounds__(kToyThreads) toy_softmax_kernel(const __grid_c
   }
 }
 
-// 4. da = (1 - h*h) * (dz @ W2.T)
+// 5. da = (1 - h*h) * (dz @ W2.T)
 __global__ void __launch_bounds__(kToyThreads) toy_dhidden_kernel(const __grid_constant__ ToyArgs a) {
   const Work w = work_of(a, blockIdx.y);
   const int k = a.batch, n_in = a.n_in, H = a.hidden, C = a.ncls;
@@ -195,14 +246,13 @@ __global__ void __launch_bounds__(kToyThreads) toy_dhidden_kernel(const __grid_c
   }
 }
 
-// 5. dW1 = x.T @ da, db1 = da.sum(0), dW2 = h.T @ dz, db2 = dz.sum(0); loss, count
+// 6. dW1 = x.T @ da, db1 = da.sum(0), dW2 = h.T @ dz, db2 = dz.sum(0); loss, count
 __global__ void __launch_bounds__(kToyThreads) toy_params_kernel(const __grid_constant__ ToyArgs a) {
   const int wk = blockIdx.y;
   const Work w = work_of(a, wk);
   const int k = a.batch, n_in = a.n_in, H = a.hidden, C = a.ncls;
   const int64_t o_b1 = static_cast<int64_t>(n_in) * H, o_w2 = o_b1 + H;
   const int64_t o_b2 = o_w2 + static_cast<int64_t>(H) * C, p = o_b2 + C;
-  const uint8_t* rec = a.records[wk];
   float* out = a.out[wk];
   TOY_LOOP(e, p + 1) {
     if (e == p) {  // the tail slots: loss sum (numpy pairwise), correct count
@@ -212,9 +262,9 @@ __global__ void __launch_bounds__(kToyThreads) toy_params_kernel(const __grid_co
     }
     double acc = 0.0;
     if (e < o_b1) {
-      const int i = static_cast<int>(e / H), j = static_cast<int>(e % H);
-      for (int r = 0; r < k; ++r)
-        acc = fma(feat(a, rec, r, i), w.da[static_cast<int64_t>(r) * H + j], acc);
+      const int64_t i = e / H, j = e % H;
+#pragma unroll 8
+      for (int r = 0; r < k; ++r) acc = fma(w.x[r * n_in + i], w.da[r * H + j], acc);
     } else if (e < o_w2) {
       const int64_t j = e - o_b1;
       for (int r = 0; r < k; ++r) acc = __dadd_rn(acc, w.da[r * H + j]);
@@ -238,9 +288,11 @@ unsigned blocks_for(int64_t elems) {
 
 }  // namespace md
 
-extern "C" int64_t md_toy_work_bytes(int32_t hidden, int32_t n_classes, int32_t batch) {
-  if (hidden < 1 || n_classes < 1 || batch < 1) return 0;
-  return 8 * md::work_doubles(batch, hidden, n_classes) * static_cast<int64_t>(MD_MAX_WORKERS);
+extern "C" int64_t md_toy_work_bytes(int32_t n_in, int32_t hidden, int32_t n_classes,
+                                     int32_t batch) {
+  if (n_in < 1 || hidden < 1 || n_classes < 1 || batch < 1) return 0;
+  return 8 * md::work_doubles(batch, n_in, hidden, n_classes) *
+         static_cast<int64_t>(MD_MAX_WORKERS);
 }
 
 extern "C" int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t n_classes,
@@ -262,7 +314,7 @@ extern "C" int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t
                   static_cast<long long>(record_stride), n_in);
     return MD_ERR_LENGTH_MISMATCH;
   }
-  const int64_t need = md_toy_work_bytes(hidden, n_classes, batch);
+  const int64_t need = md_toy_work_bytes(n_in, hidden, n_classes, batch);
   if (work_bytes < need || (reinterpret_cast<uintptr_t>(work) & 7)) {
     md::set_error("md_toy_grad: workspace of %lld bytes (need %lld, 8-byte aligned)",
                   static_cast<long long>(work_bytes), static_cast<long long>(need));
@@ -270,6 +322,18 @@ extern "C" int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t
   }
   const int64_t k = batch, H = hidden, C = n_classes;
   const int64_t p = static_cast<int64_t>(n_in) * H + H + H * C + C;
+  if (k > 65535) {
+    md::set_error("md_toy_grad: batch %d exceeds 65535 rows", batch);
+    return MD_ERR_INVALID_CONFIG;
+  }
+  // logits staging chunk: jc rows of h (float64) + W2 (float32) within 40 KB
+  const int jc = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(H, 40960 / (8 + 4 * C))));
+  const size_t smem = static_cast<size_t>(jc) * 8 + static_cast<size_t>(jc) * C * 4;
+  if (smem > 48 * 1024) {
+    md::set_error("md_toy_grad: %d classes do not fit the logits staging", n_classes);
+    return MD_ERR_INVALID_CONFIG;
+  }
   cudaStream_t s = md::as_stream(stream);
   // worker chunks run one after another on the stream, so they share the workspace
   for (int32_t w0 = 0; w0 < n_workers; w0 += MD_MAX_WORKERS) {
@@ -281,7 +345,7 @@ extern "C" int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t
     a.batch = batch;
     a.feature_bytes = feature_bytes;
     a.record_stride = record_stride;
-    a.work_stride = md::work_doubles(k, H, C);
+    a.work_stride = md::work_doubles(k, n_in, H, C);
     a.work = work;
     a.status = status;
     const int m = std::min<int32_t>(MD_MAX_WORKERS, n_workers - w0);
@@ -295,9 +359,12 @@ extern "C" int md_toy_grad(const float* w, int32_t n_in, int32_t hidden, int32_t
       }
     }
     const unsigned wm = static_cast<unsigned>(m);
-    md::toy_hidden_kernel<<<dim3(md::blocks_for(std::max(k * H, k)), wm), md::kToyThreads, 0, s>>>(a);
+    md::toy_input_kernel<<<dim3(md::blocks_for(std::max<int64_t>(k * n_in, k)), wm),
+                           md::kToyThreads, 0, s>>>(a);
     MD_LAUNCH_CHECK();
-    md::toy_logits_kernel<<<dim3(md::blocks_for(k * C), wm), md::kToyThreads, 0, s>>>(a);
+    md::toy_hidden_kernel<<<dim3(md::blocks_for(k * H), wm), md::kToyThreads, 0, s>>>(a);
+    MD_LAUNCH_CHECK();
+    md::toy_logits_kernel<<<dim3(static_cast<unsigned>(k), wm), md::kToyThreads, smem, s>>>(a, jc);
     MD_LAUNCH_CHECK();
     md::toy_softmax_kernel<<<dim3(md::blocks_for(k), wm), md::kToyThreads, 0, s>>>(a);
     MD_LAUNCH_CHECK();

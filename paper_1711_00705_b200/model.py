@@ -106,7 +106,7 @@ class ToyModel:
             raise InvalidConfig(f"expected {self.n_in} features, records hold "
                                 f"{int(recs[0].shape[1]) // feature_bytes}")
         lib = _lib.load()
-        nbytes = int(lib.md_toy_work_bytes(self.hidden, self.n_classes, k))
+        nbytes = int(lib.md_toy_work_bytes(self.n_in, self.hidden, self.n_classes, k))
         if self._work is None or self._work.numel() * 8 < nbytes \
                 or self._work.device != self.weights.device:
             self._work = torch.empty((nbytes + 7) // 8, dtype=torch.float64,
