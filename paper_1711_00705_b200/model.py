@@ -84,8 +84,9 @@ class ToyModel:
                   feature_bytes: int = 4) -> None:
         """Per-worker gradient buffers (node_gradient's layout, sgd.py:335-353):
         ``batches[j] = (records uint8 [k, L], labels int32 [k], ...)`` from the
-        DIMD batch slots, ``outs[j]`` float32 [p + 2] on the same device. One
-        launch for all workers, asynchronous on the current stream."""
+        DIMD batch slots, ``outs[j]`` float32 [p + 2] on the same device. Six
+        small launches for all workers together (up to 8 per group),
+        asynchronous on the current stream."""
         if len(batches) != len(outs) or not batches:
             raise InvalidConfig("need one output buffer per worker batch")
         recs = [b[0] for b in batches]
@@ -111,13 +112,15 @@ class ToyModel:
                 or self._work.device != self.weights.device:
             self._work = torch.empty((nbytes + 7) // 8, dtype=torch.float64,
                                      device=self.weights.device)
+        stream = torch.cuda.current_stream(self.weights.device)
+        self._work.record_stream(stream)  # a workspace reallocated later waits for this use
         _lib.check(
             lib.md_toy_grad(
                 self.weights.data_ptr(), self.n_in, self.hidden, self.n_classes,
                 _ptrs(recs), feature_bytes, _ptrs(labs), stride, k, _ptrs(outs), len(outs),
                 self._work.data_ptr(), self._work.numel() * 8,
                 None if status is None else status.data_ptr(),
-                _lib.stream_ptr(torch.cuda.current_stream(self.weights.device)),
+                _lib.stream_ptr(stream),
             )
         )
 
