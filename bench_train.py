@@ -12,6 +12,7 @@ replica check. One thread per rank, one GPU per rank when the box has enough
 GPUs (else ranks are emulated on one GPU; the line says which).
 
     python bench_train.py [--ranks 1 2 4] [--algorithms multicolor ring reduce_bcast]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench_train.py --backend torchrun
 
 Prints the reference's CSV rows (bench.py:41) and one JSON summary line. The
 reference's own numbers for the same spec on the build container's CPU come
@@ -42,7 +43,14 @@ def main() -> None:
     ap.add_argument("--hidden", type=int, default=2048)
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--backend", choices=["cuda", "torchrun"], default="cuda",
+                    help="cuda: one thread per rank in this process; torchrun: run under "
+                         "torchrun, one process per GPU (ranks = WORLD_SIZE)")
     a = ap.parse_args()
+    if a.backend == "torchrun":
+        import os
+
+        a.ranks = [int(os.environ.get("WORLD_SIZE", "1"))]
 
     import torch
 
@@ -56,10 +64,13 @@ def main() -> None:
         for n in a.ranks:
             cfg = TrainConfig(n_nodes=n, workers_per_node=a.workers, per_worker_batch=a.batch,
                               epochs=a.epochs, seed=a.seed, hidden=a.hidden)
-            emulate = n > n_gpus
+            emulate = n > n_gpus and a.backend == "cuda"
             t0 = time.perf_counter()
             try:
-                res = run_training(cfg, corpus, algo, emulate=emulate)
+                if a.backend == "torchrun":
+                    res = run_training(cfg, corpus, algo, backend="torchrun")
+                else:
+                    res = run_training(cfg, corpus, algo, emulate=emulate)
             except MinidistError as e:
                 print(f"skipping train {algo} n={n}: {e}", file=sys.stderr)
                 continue
@@ -72,7 +83,13 @@ def main() -> None:
                         "steps_per_epoch": steps, "ms_per_step": 1e3 * med / steps,
                         "epoch_s": [h.time_s for h in res.history], "final_acc": res.final_acc,
                         "final_loss": res.history[-1].loss, "wall_s": wall,
-                        "ranks": "emulated on one GPU" if emulate else "one GPU per rank"})
+                        "ranks": ("one process per GPU" if a.backend == "torchrun" else
+                                  "emulated on one GPU" if emulate else
+                                  "one GPU per rank (threads)")})
+    import os
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
     print("\n".join(rows))
     print(json.dumps({"metric": "bench_train median epoch time (reference bench.py:379-422)",
                       "unit": "s", "spec": {"records": a.records, "workers": a.workers,

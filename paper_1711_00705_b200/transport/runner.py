@@ -25,7 +25,7 @@ from paper_1711_00705_b200.transport.endpoint import (
     CudaEndpoint,
 )
 
-BACKENDS = ("cuda",)
+BACKENDS = ("cuda", "torchrun")
 
 
 @dataclass(frozen=True)
@@ -61,6 +61,10 @@ def run_ranks(
 ) -> RunResult:
     """Run ``program(endpoint)`` once per rank and collect the results.
 
+    ``"cuda"``: one host thread per rank in this process (one GPU per rank,
+    or all ranks emulated on one GPU). ``"torchrun"``: this process is one
+    rank of a job torchrun launched (one process per GPU, ``init_from_env``);
+    it runs its own rank and every process gets every rank's result.
     The reference's ``network``/``rendezvous``/``inflight_budget`` knobs
     belong to its simulated and TCP transports and have no meaning here.
     """
@@ -71,6 +75,8 @@ def run_ranks(
     for k, v in unused.items():
         if v is not None:
             raise InvalidConfig(f"{k} is not supported by the cuda backend")
+    if backend == "torchrun":
+        return _run_this_process(n_ranks, program, pull_timeout)
     mode, devices = plan_devices(n_ranks, emulate)
     board = Board(n_ranks)
     rdv = Rendezvous(n_ranks) if mode == "emulated" else None
@@ -122,6 +128,22 @@ def run_ranks(
     if any(e is not None for e in errs):
         raise next(e for e in errs if e is not None)
     return RunResult(results, None, wall)
+
+
+def _run_this_process(n_ranks: int, program, pull_timeout: float) -> RunResult:
+    ep = init_from_env(pull_timeout)
+    if ep.n_ranks != n_ranks:
+        ep.close()
+        raise InvalidConfig(f"torchrun launched {ep.n_ranks} processes, the job needs {n_ranks}")
+    t0 = time.perf_counter()
+    try:
+        with torch.cuda.stream(ep.stream):
+            res = program(ep)
+        ep.synchronize()
+        results = ep.all_gather(res)
+    finally:
+        ep.close()
+    return RunResult(results, None, time.perf_counter() - t0)
 
 
 def gpu_numa_node(device: int) -> int:

@@ -147,6 +147,23 @@ def main() -> None:
         mats = [[bytes([s, d]) * (s + d + 1) for d in range(N)] for s in range(N)]
         got = alltoallv(ep, VarPayload.from_slices(mats[rank])).data
         out["alltoallv"] = bytes(got) == b"".join(mats[s][rank] for s in range(N))
+    # 7. run_training (the reference's loop and model) with one process per
+    # rank, against the reference's own run (tests/golden/toy.npz)
+    with np.load(ROOT / "tests" / "golden" / "toy.npz") as z:
+        toy = {k: z[k] for k in z.files}
+    from paper_1711_00705_b200 import TrainConfig, make_synthetic_corpus, run_training
+
+    for t in range(int(toy["n_train"][0])):
+        nn, m, kb, epochs, seed, nrec, hidden, every, gs = (int(v) for v in toy[f"train{t}_cfg"])
+        if nn != N:
+            continue
+        cfg = TrainConfig(n_nodes=nn, workers_per_node=m, per_worker_batch=kb, epochs=epochs,
+                          seed=seed, hidden=hidden, shuffle_every=every, group_size=gs)
+        res = run_training(cfg, make_synthetic_corpus(nrec, seed=seed),
+                           str(toy[f"train{t}_algo"]), backend="torchrun")
+        steps = np.array([[s.step, s.loss, s.correct, s.lr] for s in res.steps])
+        out[f"run_training_{t}"] = bool(np.array_equal(res.weights, toy[f"train{t}_weights"])
+                                        and np.array_equal(steps, toy[f"train{t}_steps"]))
     rows = ep.all_gather(out)
     if rank == 0:
         print(json.dumps({"n": N, "ok": all(all(r.values()) for r in rows), "rows": rows}))
