@@ -110,10 +110,29 @@ def tree_config(n: int):
 # -- clocks ---------------------------------------------------------------------------------------
 
 
+# NVML poller in its own process: a thread of this process would need the GIL,
+# which the main thread holds while it launches the timed graph
+_SAMPLER = r"""
+import json, select, sys
+import pynvml as nv
+nv.nvmlInit()
+hs = [nv.nvmlDeviceGetHandleByIndex(int(i)) for i in sys.argv[1].split(",")]
+mx = max(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM) for h in hs)
+print("ready", flush=True)
+sm, mask = [], 0
+while not select.select([sys.stdin], [], [], 0.0002)[0]:
+    for h in hs:
+        sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+        mask |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+print(json.dumps({"sm": sm, "mask": mask, "max": mx}), flush=True)
+"""
+
+
 class Clocks:
     """SM clock + throttle reasons of the run's GPUs, polled through NVML (the
-    library nvidia-smi reads) every ~0.2 ms by a thread during the timed region
-    -- the region is milliseconds long, below nvidia-smi's sampling period."""
+    library nvidia-smi reads) every ~0.2 ms during the timed region -- the
+    region is milliseconds long, below nvidia-smi's sampling period. A helper
+    process polls (free of this process's GIL); a thread is the fallback."""
 
     REASONS = {  # NVML clocks-event bits -> the recipe's names
         "hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
@@ -148,21 +167,57 @@ class Clocks:
             self.ready.set()
 
     def start(self):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                [sys.executable, "-c", _SAMPLER, ",".join(str(g) for g in self.gpus)],
+                stdin=subprocess.PIPE, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            import select
+
+            if not select.select([self.proc.stdout], [], [], 30)[0] or \
+                    self.proc.stdout.readline().strip() != "ready":  # NVML initialised
+                raise RuntimeError("sampler did not start")
+            return
+        except Exception:  # noqa: BLE001  (fall back to the in-process thread)
+            if self.proc is not None:
+                self.proc.kill()
+            self.proc = None
         self.run = True
         self.t = threading.Thread(target=self._loop, daemon=True)
         self.t.start()
         self.ready.wait(timeout=30)  # NVML initialised (slow on multi-GPU boxes) before timing
         time.sleep(0.005)
 
+    def _stop_proc(self) -> bool:
+        try:
+            self.proc.stdin.write("stop\n")
+            self.proc.stdin.flush()
+            d = json.loads(self.proc.stdout.readline())
+            self.proc.wait(timeout=10)
+            self.sm = [float(x) for x in d["sm"]]
+            self.mask = int(d["mask"])
+            self.max_mhz = d["max"]
+            self.how = "helper process"
+            return True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+            self.proc.kill()
+            return False
+
     def stop(self) -> dict:
-        self.run = False
-        self.t.join(timeout=5)
+        self.how = "thread"
+        if self.proc is not None:
+            self._stop_proc()
+        else:
+            self.run = False
+            self.t.join(timeout=5)
         if self.err and not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml: {self.err}"]}
         reasons = [k for k, bit in self.REASONS.items() if self.mask & bit]
         return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.sm),
-                "source": "NVML, ~0.2 ms polling during the timed region"}
+                "source": f"NVML, ~0.2 ms polling during the timed region ({self.how})"}
 
 
 # -- our implementation ------------------------------------------------------------------------------
